@@ -1,0 +1,125 @@
+/*
+ * adaln_b200.h -- C ABI of the B200 (sm_100a) fused LayerNorm-Modulate (AdaLN) operator.
+ *
+ * This is the drop-in boundary under the reference's Python operator API
+ * (`adaptiveload.adaln`, /root/reference/pkg/src/adaptiveload/adaln/__init__.py).
+ * The reference selects a backend module exposing
+ *     forward(x, scale, shift, eps) -> (y, mu, rstd)                 _kernels_numba.py:37-42
+ *     backward_dx(dy, x, scale, mu, rstd) -> dx                       _kernels_numba.py:65-68
+ *     backward_naive(dy, x, scale, mu, rstd) -> (dx, dscale, dshift)  _kernels_numba.py:86-91
+ *     dtile_reduce(dy, x, mu, rstd, d_tile, n_tile, fp32_accum)       _kernels_numba.py:130-137
+ * (chosen once by _select_backend, adaln/__init__.py:38-53).  The entry points below replace
+ * that module: al_adaln_forward replaces `forward`; al_adaln_backward replaces
+ * `backward_naive` and `dtile_reduce` + `backward_dx` (dx and dscale/dshift in one pass).
+ *
+ * Conventions
+ *  - Plain pointers to DEVICE memory, sizes in elements, no torch types.  The library never
+ *    allocates or frees: the caller owns every output and the workspace.
+ *  - All work is stream-ordered on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *    default stream).  Calls are asynchronous; nothing synchronises the host.
+ *  - Layout: x, y, dy, dx are row-major [batch, seq, dim] (= [N, dim] rows, N = batch*seq).
+ *    scale/shift are [batch, dim] with row stride `mod_stride` elements (mod_stride = dim for
+ *    per-sample modulation, 0 to broadcast one [dim] vector over every row -- the reference's
+ *    2-D case, adaln/__init__.py:88-96).
+ *  - dtype codes: AL_F32, AL_BF16, AL_F16 compute in fp32; AL_F64 computes in fp64.
+ *    mean/rstd/dscale/dshift are fp32 for the 16/32-bit dtypes and fp64 for AL_F64.
+ *  - dscale/dshift are [batch, dim] when mod_stride != 0, else [dim] (summed over all rows).
+ *  - `nonfinite` (device int*, may be NULL): set to 1 by the kernels if an input they validate
+ *    (x/scale/shift in forward; dy/x/scale in backward) holds NaN/Inf.  This folds the
+ *    reference's `_as_f64` isfinite scan (adaln/__init__.py:81-85) into the single HBM pass;
+ *    the caller checks it when it wants the reference's NonFiniteInput behaviour.
+ *  - Results are deterministic: fixed CTA->row mapping and a fixed stage-2 reduction order
+ *    (SPEC.md:462), so repeated calls are bit-identical.
+ */
+#ifndef ADALN_B200_H_
+#define ADALN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define AL_API __attribute__((visibility("default")))
+#else
+#define AL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python layer maps them onto the reference exception types (errors.py:72-85) */
+#define AL_OK 0
+#define AL_ERR_SHAPE 1      /* ShapeMismatch   (adaln/__init__.py:90,93,127,149)        */
+#define AL_ERR_TILE 3       /* InvalidTile     (adaln/__init__.py:151-153)              */
+#define AL_ERR_VALUE 5      /* ValueError      (eps <= 0, adaln/__init__.py:105-106)    */
+#define AL_ERR_DTYPE 6      /* unsupported dtype code                                    */
+#define AL_ERR_WORKSPACE 7  /* workspace too small / NULL                                */
+#define AL_ERR_CUDA 8       /* CUDA runtime error; al_last_error() has the text         */
+
+/* dtype codes */
+#define AL_F32 0
+#define AL_BF16 1
+#define AL_F16 2
+#define AL_F64 3
+
+/* ABI version of this header (bumped on any signature change). */
+AL_API int al_abi_version(void);
+
+/* Human-readable message for the last error on the calling thread. */
+AL_API const char* al_last_error(void);
+
+/* Optional: load every kernel image and set its shared-memory attribute on `device`, so later
+ * calls are safe inside CUDA-graph capture.  Called lazily by the first launch otherwise. */
+AL_API int al_device_init(int device);
+
+/*
+ * Forward: y = (x - mu) * rstd * (1 + scale) + shift, mu/rstd per row (population variance,
+ * eps inside the sqrt), one HBM read of x and one write of y + mean + rstd.
+ * Replaces _kernels_numba.forward / _forward_kernel (_kernels_numba.py:18-42) and the
+ * per-call validation of adaln_forward (adaln/__init__.py:99-108).
+ */
+AL_API int al_adaln_forward(const void* x, const void* scale, const void* shift,
+                     void* y, void* mean, void* rstd,
+                     int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
+                     int dtype, double eps, int* nonfinite, void* stream);
+
+/* Bytes of scratch al_adaln_backward needs for the stage-1 (per-CTA) dscale/dshift partials. */
+AL_API int64_t al_adaln_backward_workspace_bytes(int64_t batch, int64_t seq, int64_t dim,
+                                          int64_t mod_stride, int dtype, int64_t n_tile);
+
+/*
+ * Backward: dx (_backward_dx_kernel, _kernels_numba.py:45-62) and dscale/dshift
+ * (_reduce_naive_kernel :71-83 / _dtile_kernel_* :94-127) in one pass over dy and x.
+ * Stage 1: each CTA owns a contiguous row range and every thread owns fixed feature columns
+ * (the paper's D-tile mapping); per-column fp32 partials go to `workspace`.  Stage 2: a second
+ * kernel sums the partials over CTAs in ascending CTA order (fp64 accumulator).
+ * d_tile / n_tile: the reference TileConfig (adaln/__init__.py:70-73), validated with the
+ * reference bounds (1 <= d_tile <= dim, 1 <= n_tile <= rows per reduction group); n_tile caps
+ * the rows per stage-1 partial; 0/0 selects the default tiling (adaln_backward_naive).
+ */
+AL_API int al_adaln_backward(const void* dy, const void* x, const void* scale,
+                      const void* mean, const void* rstd,
+                      void* dx, void* dscale, void* dshift,
+                      void* workspace, int64_t workspace_bytes,
+                      int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
+                      int dtype, int64_t d_tile, int64_t n_tile,
+                      int* nonfinite, void* stream);
+
+/*
+ * Tuning overrides for benchmarking sweeps (0 = automatic).  kernel: 0 = forward, 1 = backward.
+ * vecs_per_thread in {1,2,4}; rows_per_stage in {1,2,4}; smem_budget in bytes per CTA;
+ * force_generic = 1 routes through the generic (any-shape) kernels.  Process-global.
+ */
+AL_API int al_set_tuning(int kernel, int vecs_per_thread, int rows_per_stage, int smem_budget,
+                  int force_generic);
+
+/* Describe the launch al_adaln_{forward,backward} would use: writes
+ * {path(0 generic,1 tma), grid, threads, vecs_per_thread, rows_per_stage, stages, smem_bytes}. */
+AL_API int al_describe_launch(int kernel, int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
+                       int dtype, int64_t n_tile, int64_t out[7]);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADALN_B200_H_ */

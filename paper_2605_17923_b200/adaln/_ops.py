@@ -1,0 +1,151 @@
+"""Device-level entry points: torch CUDA tensors in, torch CUDA tensors out.
+
+These are the thin host-side callers of the C ABI (``include/adaln_b200.h``).  Torch is only
+plumbing here: it owns the device memory (caching allocator) and the current stream; all
+arithmetic runs in the sm_100a kernels of ``libadaln_b200.so``.
+
+Layouts accepted (the reference accepts only the first, adaln/__init__.py:88-96):
+  * x [N, D] with scale/shift [D]            -> mean/rstd [N],    dscale/dshift [D]
+  * x [B, S, D] with scale/shift [B, D]      -> mean/rstd [B, S], dscale/dshift [B, D]
+  * x [B, S, D] with scale/shift [D]         -> mean/rstd [B, S], dscale/dshift [D]
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from .. import _native as nat
+from ..errors import NonFiniteInput, ShapeMismatch
+
+_DTYPE_CODE = {
+    torch.float32: nat.AL_F32,
+    torch.bfloat16: nat.AL_BF16,
+    torch.float16: nat.AL_F16,
+    torch.float64: nat.AL_F64,
+}
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    try:
+        return _DTYPE_CODE[dt]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {dt}; expected float32/bfloat16/float16/float64") from None
+
+
+def stat_dtype(dt: torch.dtype) -> torch.dtype:
+    """mean/rstd/dscale/dshift dtype: fp64 for fp64 inputs, fp32 otherwise."""
+    return torch.float64 if dt == torch.float64 else torch.float32
+
+
+@dataclass(frozen=True)
+class Geometry:
+    batch: int
+    seq: int
+    dim: int
+    mod_stride: int  # 0 = scale/shift broadcast over every row
+    stats_shape: tuple
+    grad_shape: tuple
+
+
+def geometry(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor | None = None) -> Geometry:
+    if x.dim() == 2:
+        n, d = x.shape
+        b, s = 1, n
+        stats_shape = (n,)
+    elif x.dim() == 3:
+        b, s, d = x.shape
+        stats_shape = (b, s)
+    else:
+        raise ShapeMismatch(f"x must be 2-D [N, D] or 3-D [B, S, D], got {tuple(x.shape)}")
+    mods = [scale] if shift is None else [scale, shift]
+    shapes = [tuple(m.shape) for m in mods]
+    if all(sh == (d,) for sh in shapes):
+        return Geometry(b, s, d, 0, stats_shape, (d,))
+    if x.dim() == 3 and all(sh == (b, d) for sh in shapes):
+        return Geometry(b, s, d, d, stats_shape, (b, d))
+    want = f"({d},)" if x.dim() == 2 else f"({d},) or ({b}, {d})"
+    raise ShapeMismatch(f"scale/shift must have shape {want}, got {shapes}")
+
+
+def _stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _prep(t: torch.Tensor, dt: torch.dtype, device: torch.device) -> torch.Tensor:
+    if t.device != device:
+        raise ShapeMismatch(f"all tensors must be on {device}, got {t.device}")
+    if t.dtype != dt:
+        t = t.to(dt)
+    return t.contiguous()
+
+
+def _raise_if_flagged(flag: torch.Tensor | None, what: str) -> None:
+    if flag is not None and int(flag.item()) != 0:
+        raise NonFiniteInput(f"{what} contains NaN or Inf")
+
+
+def fused_forward(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor, eps: float = 1e-6,
+                  *, check_finite: bool = False, out: torch.Tensor | None = None):
+    """y, mean, rstd = AdaLN forward (one HBM pass).  Asynchronous unless check_finite."""
+    if not x.is_cuda:
+        raise ShapeMismatch("fused_forward takes CUDA tensors; use adaln_forward for host data")
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    g = geometry(x, scale, shift)
+    dev = x.device
+    nat.ensure_device(dev.index)
+    x = _prep(x, x.dtype, dev)
+    scale = _prep(scale, x.dtype, dev)
+    shift = _prep(shift, x.dtype, dev)
+    y = torch.empty_like(x) if out is None else out
+    sdt = stat_dtype(x.dtype)
+    mean = torch.empty(g.stats_shape, dtype=sdt, device=dev)
+    rstd = torch.empty(g.stats_shape, dtype=sdt, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
+    rc = nat.load().al_adaln_forward(
+        x.data_ptr(), scale.data_ptr(), shift.data_ptr(), y.data_ptr(), mean.data_ptr(),
+        rstd.data_ptr(), g.batch, g.seq, g.dim, g.mod_stride, dtype_code(x.dtype), float(eps),
+        flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
+    nat.check(rc, "al_adaln_forward")
+    _raise_if_flagged(flag, "x/scale/shift")
+    return y, mean, rstd
+
+
+def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean: torch.Tensor,
+                   rstd: torch.Tensor, *, d_tile: int = 0, n_tile: int = 0,
+                   check_finite: bool = False):
+    """dx, dscale, dshift in one pass over (dy, x) + a deterministic cross-CTA reduction."""
+    if not x.is_cuda:
+        raise ShapeMismatch("fused_backward takes CUDA tensors; use adaln_backward_* for host data")
+    g = geometry(x, scale)
+    if tuple(dy.shape) != tuple(x.shape):
+        raise ShapeMismatch(f"dy shape {tuple(dy.shape)} != x shape {tuple(x.shape)}")
+    dev = x.device
+    nat.ensure_device(dev.index)
+    x = _prep(x, x.dtype, dev)
+    dy = _prep(dy, x.dtype, dev)
+    scale = _prep(scale, x.dtype, dev)
+    sdt = stat_dtype(x.dtype)
+    mean = _prep(mean, sdt, dev)
+    rstd = _prep(rstd, sdt, dev)
+    lib = nat.load()
+    code = dtype_code(x.dtype)
+    ws_bytes = lib.al_adaln_backward_workspace_bytes(g.batch, g.seq, g.dim, g.mod_stride, code,
+                                                     n_tile)
+    if ws_bytes < 0:
+        nat.check(nat.AL_ERR_SHAPE, "al_adaln_backward_workspace_bytes")
+    ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
+    dx = torch.empty_like(x)
+    dscale = torch.empty(g.grad_shape, dtype=sdt, device=dev)
+    dshift = torch.empty(g.grad_shape, dtype=sdt, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
+    rc = lib.al_adaln_backward(
+        dy.data_ptr(), x.data_ptr(), scale.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+        dx.data_ptr(), dscale.data_ptr(), dshift.data_ptr(), ws.data_ptr(), int(ws_bytes),
+        g.batch, g.seq, g.dim, g.mod_stride, code, d_tile, n_tile,
+        flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
+    nat.check(rc, "al_adaln_backward")
+    _raise_if_flagged(flag, "dy/x/scale")
+    return dx, dscale, dshift

@@ -1,0 +1,464 @@
+// adaln_capi.cu -- C ABI (include/adaln_b200.h) over the sm_100a AdaLN kernels: argument
+// validation with the reference's error taxonomy, launch planning (vector width, ring depth,
+// grid = SMs x resident CTAs), and dispatch.  The library never allocates.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+
+#include "../../include/adaln_b200.h"
+#include "adaln_kernels.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(AL_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+// ---------------------------------------------------------------- tuning
+struct Tuning {
+  int V = 0, R = 0, smem_budget = 0, force_generic = 0;
+};
+Tuning g_tune[2];
+std::mutex g_mu;
+
+constexpr int kMaxThreads = 512;        // __launch_bounds__ of the TMA kernels
+constexpr int kSmemOptin = 227 * 1024;  // sm_100 per-CTA opt-in maximum
+constexpr int kDefaultBudget[2] = {100 * 1024, 100 * 1024};
+constexpr int kDefaultR[2] = {2, 2};
+
+// ---------------------------------------------------------------- device info
+struct DevInfo {
+  int sms = 0;
+  bool init = false;
+};
+DevInfo g_dev[64];
+
+int current_device(int* dev) {
+  cudaError_t e = cudaGetDevice(dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (*dev < 0 || *dev >= 64) return fail(AL_ERR_CUDA, "device ordinal %d out of range", *dev);
+  return AL_OK;
+}
+
+int dev_sms(int dev, int* sms) {
+  if (!g_dev[dev].init) {
+    int v = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    g_dev[dev].sms = v;
+    g_dev[dev].init = true;
+  }
+  *sms = g_dev[dev].sms;
+  return AL_OK;
+}
+
+// ---------------------------------------------------------------- kernel tables
+using FwdFn = void (*)(al::FwdParams);
+using BwdFn = void (*)(al::BwdParams);
+
+template <typename T>
+struct Table {
+  FwdFn fwd[3][3];  // [V idx][R idx], V in {1,2,4}, R in {1,2,4}
+  BwdFn bwd[3][3];
+  FwdFn fwd_generic;
+  BwdFn bwd_generic;
+  Table() {
+    fwd[0][0] = al::adaln_fwd_tma<T, 1, 1>;
+    fwd[0][1] = al::adaln_fwd_tma<T, 1, 2>;
+    fwd[0][2] = al::adaln_fwd_tma<T, 1, 4>;
+    fwd[1][0] = al::adaln_fwd_tma<T, 2, 1>;
+    fwd[1][1] = al::adaln_fwd_tma<T, 2, 2>;
+    fwd[1][2] = al::adaln_fwd_tma<T, 2, 4>;
+    fwd[2][0] = al::adaln_fwd_tma<T, 4, 1>;
+    fwd[2][1] = al::adaln_fwd_tma<T, 4, 2>;
+    fwd[2][2] = al::adaln_fwd_tma<T, 4, 4>;
+    bwd[0][0] = al::adaln_bwd_tma<T, 1, 1>;
+    bwd[0][1] = al::adaln_bwd_tma<T, 1, 2>;
+    bwd[0][2] = al::adaln_bwd_tma<T, 1, 4>;
+    bwd[1][0] = al::adaln_bwd_tma<T, 2, 1>;
+    bwd[1][1] = al::adaln_bwd_tma<T, 2, 2>;
+    bwd[1][2] = al::adaln_bwd_tma<T, 2, 4>;
+    bwd[2][0] = al::adaln_bwd_tma<T, 4, 1>;
+    bwd[2][1] = al::adaln_bwd_tma<T, 4, 2>;
+    bwd[2][2] = al::adaln_bwd_tma<T, 4, 4>;
+    fwd_generic = al::adaln_fwd_generic<T>;
+    bwd_generic = al::adaln_bwd_generic<T>;
+  }
+};
+
+const Table<float> t_f32;
+const Table<__nv_bfloat16> t_bf16;
+const Table<__half> t_f16;
+const Table<double> t_f64;
+
+int vidx(int V) { return V == 1 ? 0 : (V == 2 ? 1 : 2); }
+
+int elem_size(int dtype) {
+  switch (dtype) {
+    case AL_F32: return 4;
+    case AL_BF16: return 2;
+    case AL_F16: return 2;
+    case AL_F64: return 8;
+    default: return 0;
+  }
+}
+int ct_size(int dtype) { return dtype == AL_F64 ? 8 : 4; }
+
+const void* tma_kernel(int kernel, int dtype, int V, int R) {
+  const int a = vidx(V), b = vidx(R);
+  switch (dtype) {
+    case AL_F32: return kernel ? (const void*)t_f32.bwd[a][b] : (const void*)t_f32.fwd[a][b];
+    case AL_BF16: return kernel ? (const void*)t_bf16.bwd[a][b] : (const void*)t_bf16.fwd[a][b];
+    case AL_F16: return kernel ? (const void*)t_f16.bwd[a][b] : (const void*)t_f16.fwd[a][b];
+    case AL_F64: return kernel ? (const void*)t_f64.bwd[a][b] : (const void*)t_f64.fwd[a][b];
+  }
+  return nullptr;
+}
+const void* generic_kernel(int kernel, int dtype) {
+  switch (dtype) {
+    case AL_F32: return kernel ? (const void*)t_f32.bwd_generic : (const void*)t_f32.fwd_generic;
+    case AL_BF16: return kernel ? (const void*)t_bf16.bwd_generic : (const void*)t_bf16.fwd_generic;
+    case AL_F16: return kernel ? (const void*)t_f16.bwd_generic : (const void*)t_f16.fwd_generic;
+    case AL_F64: return kernel ? (const void*)t_f64.bwd_generic : (const void*)t_f64.fwd_generic;
+  }
+  return nullptr;
+}
+const void* reduce_kernel(int dtype) {
+  return dtype == AL_F64 ? (const void*)al::adaln_bwd_reduce<double>
+                         : (const void*)al::adaln_bwd_reduce<float>;
+}
+
+// Per-(kernel image, device) one-time attribute setup.
+struct AttrCache {
+  std::mutex mu;
+  const void* fn[512];
+  int dev[512];
+  int n = 0;
+};
+AttrCache g_attr;
+
+int ensure_attr(const void* fn, int dev) {
+  std::lock_guard<std::mutex> lk(g_attr.mu);
+  for (int i = 0; i < g_attr.n; ++i)
+    if (g_attr.fn[i] == fn && g_attr.dev[i] == dev) return AL_OK;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  if (g_attr.n < 512) {
+    g_attr.fn[g_attr.n] = fn;
+    g_attr.dev[g_attr.n] = dev;
+    ++g_attr.n;
+  }
+  return AL_OK;
+}
+
+// ---------------------------------------------------------------- launch planning
+struct Plan {
+  int path = 0;  // 0 generic, 1 tma
+  int grid = 0, threads = 0, V = 0, R = 0, NS = 0;
+  size_t smem = 0;
+  const void* fn = nullptr;
+};
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// kernel: 0 fwd, 1 bwd.  `ptrs` are the row-tensor / modulation pointers that the vector path
+// reads or writes with 16-byte accesses.
+int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, int64_t n_tile,
+              const void* const* ptrs, int nptrs, Plan* out, bool force_generic = false) {
+  int dev, sms;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  rc = dev_sms(dev, &sms);
+  if (rc) return rc;
+  Tuning tu;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    tu = g_tune[kernel];
+  }
+  const int es = elem_size(dtype);
+  const int cs = ct_size(dtype);
+  const int epv = 16 / es;
+  bool vec_ok = !tu.force_generic && !force_generic && (D * es) % 16 == 0 && (mod_stride * es) % 16 == 0;
+  for (int i = 0; i < nptrs && vec_ok; ++i) vec_ok = aligned16(ptrs[i]);
+  Plan pl;
+  if (vec_ok) {
+    const int64_t nvec = D / epv;
+    const int row_bytes = static_cast<int>(D * es);
+    const int vcap = kernel ? 384 : 256;
+    int V = tu.V;
+    if (V == 0) {
+      V = 4;
+      for (int v : {1, 2, 4})
+        if (((nvec + v - 1) / v + 31) / 32 * 32 <= vcap) {
+          V = v;
+          break;
+        }
+    }
+    const int64_t nc = ((nvec + V - 1) / V + 31) / 32 * 32;
+    const int budget = tu.smem_budget ? tu.smem_budget : kDefaultBudget[kernel];
+    int R = tu.R ? tu.R : kDefaultR[kernel];
+    const int tensors = kernel ? 2 : 1;
+    int NS = 0;
+    size_t smem = 0;
+    while (true) {
+      const int64_t stage = static_cast<int64_t>(tensors) * R * row_bytes;
+      int64_t ns = budget / stage;
+      if (ns > 8) ns = 8;
+      if (ns < 2 && stage * 2 <= kSmemOptin - 4096) ns = 2;
+      const int ncw = static_cast<int>(nc / 32);
+      const size_t extra = 16 * static_cast<size_t>(ns) + (2 * ncw * R * 2 + ncw) * cs + 64;
+      if (ns >= 2 && static_cast<size_t>(ns * stage) + extra <= static_cast<size_t>(kSmemOptin)) {
+        NS = static_cast<int>(ns);
+        smem = static_cast<size_t>(ns * stage) + extra;
+        break;
+      }
+      if (R == 1) break;
+      R /= 2;
+    }
+    if (nc + 32 <= kMaxThreads && NS >= 2 && (V == 1 || V == 2 || V == 4) &&
+        (R == 1 || R == 2 || R == 4)) {
+      pl.path = 1;
+      pl.V = V;
+      pl.R = R;
+      pl.NS = NS;
+      pl.threads = static_cast<int>(nc) + 32;
+      pl.smem = smem;
+      pl.fn = tma_kernel(kernel, dtype, V, R);
+      rc = ensure_attr(pl.fn, dev);
+      if (rc) return rc;
+      int occ = 0;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pl.fn, pl.threads, pl.smem);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+      if (occ < 1) pl.path = 0;
+      else pl.grid = static_cast<int>(std::min<int64_t>(N, static_cast<int64_t>(sms) * occ));
+    }
+  }
+  if (pl.path == 0) {
+    pl = Plan();
+    pl.threads = 256;
+    pl.fn = generic_kernel(kernel, dtype);
+    int64_t grid;
+    if (kernel == 0) grid = std::min<int64_t>((N + 7) / 8, static_cast<int64_t>(sms) * 8);
+    else grid = std::min<int64_t>(N, static_cast<int64_t>(sms) * 4);
+    pl.grid = static_cast<int>(std::max<int64_t>(grid, 1));
+  }
+  if (kernel == 1 && n_tile > 0) {
+    // n_tile caps the rows folded into one stage-1 partial (bounded to keep the workspace sane)
+    const int64_t want = (N + n_tile - 1) / n_tile;
+    const int64_t cap = std::max<int64_t>(pl.grid, std::min<int64_t>(N, 8192));
+    pl.grid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(pl.grid, want), cap));
+  }
+  *out = pl;
+  return AL_OK;
+}
+
+int check_common(int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride, int dtype) {
+  if (elem_size(dtype) == 0) return fail(AL_ERR_DTYPE, "unsupported dtype code %d", dtype);
+  if (batch < 0 || seq < 0) return fail(AL_ERR_SHAPE, "batch/seq must be >= 0");
+  if (dim < 1) return fail(AL_ERR_SHAPE, "dim must be >= 1, got %lld", (long long)dim);
+  if (mod_stride != 0 && mod_stride < dim)
+    return fail(AL_ERR_SHAPE, "mod_stride must be 0 or >= dim");
+  if (batch * seq > 0 && (dim > (int64_t(1) << 31) / 8))
+    return fail(AL_ERR_SHAPE, "dim too large");
+  return AL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int al_abi_version(void) { return 1; }
+
+const char* al_last_error(void) { return g_err; }
+
+int al_set_tuning(int kernel, int vecs_per_thread, int rows_per_stage, int smem_budget,
+                  int force_generic) {
+  if (kernel < 0 || kernel > 1) return fail(AL_ERR_VALUE, "kernel must be 0 or 1");
+  if (vecs_per_thread && vecs_per_thread != 1 && vecs_per_thread != 2 && vecs_per_thread != 4)
+    return fail(AL_ERR_VALUE, "vecs_per_thread must be 0,1,2,4");
+  if (rows_per_stage && rows_per_stage != 1 && rows_per_stage != 2 && rows_per_stage != 4)
+    return fail(AL_ERR_VALUE, "rows_per_stage must be 0,1,2,4");
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_tune[kernel].V = vecs_per_thread;
+  g_tune[kernel].R = rows_per_stage;
+  g_tune[kernel].smem_budget = smem_budget;
+  g_tune[kernel].force_generic = force_generic;
+  return AL_OK;
+}
+
+int al_device_init(int device) {
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  int sms;
+  int rc = dev_sms(device, &sms);
+  if (rc) return rc;
+  for (int dt = 0; dt < 4; ++dt) {
+    for (int kernel = 0; kernel < 2; ++kernel) {
+      for (int V : {1, 2, 4})
+        for (int R : {1, 2, 4}) {
+          rc = ensure_attr(tma_kernel(kernel, dt, V, R), device);
+          if (rc) return rc;
+        }
+      cudaFuncAttributes fa;
+      e = cudaFuncGetAttributes(&fa, generic_kernel(kernel, dt));
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+    }
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, reduce_kernel(dt));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+  }
+  return AL_OK;
+}
+
+int al_describe_launch(int kernel, int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
+                       int dtype, int64_t n_tile, int64_t out[7]) {
+  int rc = check_common(batch, seq, dim, mod_stride, dtype);
+  if (rc) return rc;
+  if (kernel < 0 || kernel > 1) return fail(AL_ERR_VALUE, "kernel must be 0 or 1");
+  Plan pl;
+  const void* aligned[1] = {reinterpret_cast<const void*>(uintptr_t(256))};
+  rc = make_plan(kernel, batch * seq, dim, mod_stride, dtype, n_tile, aligned, 1, &pl);
+  if (rc) return rc;
+  out[0] = pl.path;
+  out[1] = pl.grid;
+  out[2] = pl.threads;
+  out[3] = pl.V;
+  out[4] = pl.R;
+  out[5] = pl.NS;
+  out[6] = static_cast<int64_t>(pl.smem);
+  return AL_OK;
+}
+
+int al_adaln_forward(const void* x, const void* scale, const void* shift, void* y, void* mean,
+                     void* rstd, int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
+                     int dtype, double eps, int* nonfinite, void* stream) {
+  int rc = check_common(batch, seq, dim, mod_stride, dtype);
+  if (rc) return rc;
+  if (!(eps > 0.0)) return fail(AL_ERR_VALUE, "eps must be positive");
+  const int64_t N = batch * seq;
+  if (N == 0) return AL_OK;
+  if (!x || !scale || !shift || !y || !mean || !rstd)
+    return fail(AL_ERR_SHAPE, "null tensor pointer");
+  const void* vp[4] = {x, y, scale, shift};
+  Plan pl;
+  rc = make_plan(0, N, dim, mod_stride, dtype, 0, vp, 4, &pl);
+  if (rc) return rc;
+  al::FwdParams p;
+  p.x = x;
+  p.scale = scale;
+  p.shift = shift;
+  p.y = y;
+  p.mean = mean;
+  p.rstd = rstd;
+  p.N = N;
+  p.S_grp = mod_stride ? seq : N;
+  p.D = dim;
+  p.mod_stride = mod_stride;
+  p.eps = eps;
+  p.nonfinite = nonfinite;
+  p.nvec = static_cast<int>(dim * elem_size(dtype) / 16);
+  p.row_bytes = static_cast<int>(dim * elem_size(dtype));
+  p.nstages = pl.NS;
+  p.G = pl.grid;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* args[] = {&p};
+  cudaError_t e = cudaLaunchKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st);
+  if (e != cudaSuccess) return cuda_fail(e, "forward launch");
+  return AL_OK;
+}
+
+int64_t al_adaln_backward_workspace_bytes(int64_t batch, int64_t seq, int64_t dim,
+                                          int64_t mod_stride, int dtype, int64_t n_tile) {
+  if (check_common(batch, seq, dim, mod_stride, dtype)) return -1;
+  const int64_t N = batch * seq;
+  if (N == 0) return 0;
+  // the larger of the vector-path and generic-path plans, so any pointer alignment fits
+  Plan pa, pg;
+  const void* aligned[1] = {reinterpret_cast<const void*>(uintptr_t(256))};
+  if (make_plan(1, N, dim, mod_stride, dtype, n_tile, aligned, 1, &pa)) return -1;
+  if (make_plan(1, N, dim, mod_stride, dtype, n_tile, aligned, 1, &pg, true)) return -1;
+  const int64_t ngroups = mod_stride ? batch : 1;
+  return 2 * (std::max(pa.grid, pg.grid) + ngroups - 1) * dim * ct_size(dtype);
+}
+
+int al_adaln_backward(const void* dy, const void* x, const void* scale, const void* mean,
+                      const void* rstd, void* dx, void* dscale, void* dshift, void* workspace,
+                      int64_t workspace_bytes, int64_t batch, int64_t seq, int64_t dim,
+                      int64_t mod_stride, int dtype, int64_t d_tile, int64_t n_tile,
+                      int* nonfinite, void* stream) {
+  int rc = check_common(batch, seq, dim, mod_stride, dtype);
+  if (rc) return rc;
+  const int64_t N = batch * seq;
+  const int64_t S_grp = mod_stride ? seq : N;
+  const int64_t ngroups = mod_stride ? batch : 1;
+  if (d_tile != 0 || n_tile != 0) {
+    if (!(d_tile >= 1 && d_tile <= dim && n_tile >= 1 && n_tile <= S_grp))
+      return fail(AL_ERR_TILE, "tile config (d_tile=%lld, n_tile=%lld) out of bounds for N=%lld, D=%lld",
+                  (long long)d_tile, (long long)n_tile, (long long)S_grp, (long long)dim);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (N == 0) {
+    if (ngroups > 0 && dscale && dshift) {
+      cudaError_t e = cudaMemsetAsync(dscale, 0, ngroups * dim * ct_size(dtype), st);
+      if (e == cudaSuccess) e = cudaMemsetAsync(dshift, 0, ngroups * dim * ct_size(dtype), st);
+      if (e != cudaSuccess) return cuda_fail(e, "memset");
+    }
+    return AL_OK;
+  }
+  if (!dy || !x || !scale || !mean || !rstd || !dx || !dscale || !dshift)
+    return fail(AL_ERR_SHAPE, "null tensor pointer");
+  const void* vp[5] = {dy, x, scale, dx, workspace};
+  Plan pl;
+  rc = make_plan(1, N, dim, mod_stride, dtype, n_tile, vp, 5, &pl);
+  if (rc) return rc;
+  const int64_t nslots = pl.grid + ngroups - 1;
+  const int64_t need = 2 * nslots * dim * ct_size(dtype);
+  if (!workspace || workspace_bytes < need) {
+    return fail(AL_ERR_WORKSPACE, "workspace too small: need %lld bytes, got %lld",
+                (long long)need, (long long)workspace_bytes);
+  }
+  al::BwdParams p;
+  p.dy = dy;
+  p.x = x;
+  p.scale = scale;
+  p.mean = mean;
+  p.rstd = rstd;
+  p.dx = dx;
+  p.ws = workspace;
+  p.N = N;
+  p.S_grp = S_grp;
+  p.D = dim;
+  p.mod_stride = mod_stride;
+  p.nslots = nslots;
+  p.nonfinite = nonfinite;
+  p.nvec = static_cast<int>(dim * elem_size(dtype) / 16);
+  p.row_bytes = static_cast<int>(dim * elem_size(dtype));
+  p.nstages = pl.NS;
+  p.G = pl.grid;
+  void* args[] = {&p};
+  cudaError_t e = cudaLaunchKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st);
+  if (e != cudaSuccess) return cuda_fail(e, "backward stage-1 launch");
+  const void* rk = reduce_kernel(dtype);
+  int64_t G64 = pl.grid;
+  void* rargs[] = {&workspace, &dscale, &dshift, &p.N, &p.S_grp, &p.D, &G64, &p.nslots};
+  dim3 rgrid(static_cast<unsigned>((dim + 31) / 32), static_cast<unsigned>(ngroups));
+  e = cudaLaunchKernel(rk, rgrid, dim3(256), rargs, 0, st);
+  if (e != cudaSuccess) return cuda_fail(e, "backward stage-2 launch");
+  return AL_OK;
+}
+
+}  // extern "C"

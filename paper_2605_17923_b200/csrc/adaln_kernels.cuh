@@ -1,0 +1,683 @@
+// adaln_kernels.cuh -- sm_100a kernels of the fused LayerNorm-Modulate (AdaLN) operator.
+//
+// Reference arithmetic (f64 CPU oracle, /root/reference/pkg/src/adaptiveload/adaln/):
+//   forward   _kernels_numba.py:18-34   mu = sum(x)/D; var = sum((x-mu)^2)/D;
+//                                       rstd = 1/sqrt(var+eps); y = (x-mu)*rstd*(1+scale)+shift
+//   dx        _kernels_numba.py:45-62   g = dy*(1+scale); dx = rstd*(g - mean(g) - xhat*mean(g*xhat))
+//   dscale/dshift _kernels_numba.py:71-83 (naive) / :94-127 (d-tile): column sums over the
+//                                       sequence of dy*xhat and dy.
+//
+// Design (bandwidth-bound; tensor cores deliberately unused):
+//  * Persistent-style static row partition: CTA k owns rows [k*N/G, (k+1)*N/G).  Rows are
+//    streamed through an NS-stage shared-memory ring by 1-D TMA bulk copies (cp.async.bulk)
+//    issued by one producer lane; mbarrier full/empty pairs decouple copy and compute, so
+//    HBM reads stay in flight while consumers reduce and write.
+//  * Consumer thread t owns 16-byte column vectors t + i*nc (i < V): the paper's
+//    "thread fixed to feature d" D-tile mapping.  Shared-memory reads are
+//    conflict-free 128-bit loads, global writes are coalesced 128-bit streaming stores, and the
+//    per-column (1+scale), shift and dscale/dshift accumulators live in registers.
+//  * Forward statistics: exact per-thread two-pass (mean, M2) over the owned elements, merged
+//    across lanes and warps with the parallel-variance identity
+//        M2 = sum_i [M2_i + n_i (m_i - m)^2],  m = sum_i n_i m_i / n,
+//    i.e. Welford/Chan merging: one reduction round per stage, no E[x^2]-E[x]^2 cancellation.
+//  * Backward: stage 1 (this kernel) writes per-CTA fp32 column partials of dy*xhat and dy;
+//    stage 2 (adaln_bwd_reduce) sums them over CTAs in ascending CTA order in fp64.
+//    Deterministic: no floating-point atomics anywhere.
+//  * A stage never straddles a modulation/reduction group (sample), so scale/shift and the
+//    partial accumulators are constant within a stage.
+#pragma once
+#include <cstdint>
+
+#include "dtype.cuh"
+#include "ptx.cuh"
+
+namespace al {
+
+struct FwdParams {
+  const void* x;
+  const void* scale;
+  const void* shift;
+  void* y;
+  void* mean;
+  void* rstd;
+  int64_t N;           // rows (batch * seq)
+  int64_t S_grp;       // rows per modulation group (seq, or N when scale/shift broadcast)
+  int64_t D;           // features
+  int64_t mod_stride;  // elements between consecutive groups' scale/shift rows
+  double eps;
+  int* nonfinite;
+  int nvec;       // D / EPV
+  int row_bytes;  // D * sizeof(T)
+  int nstages;    // ring depth
+  int G;          // CTAs
+};
+
+struct BwdParams {
+  const void* dy;
+  const void* x;
+  const void* scale;
+  const void* mean;
+  const void* rstd;
+  void* dx;
+  void* ws;  // [2][nslots][D] partials (dscale | dshift), compute type
+  int64_t N;
+  int64_t S_grp;  // rows per reduction group (seq, or N when scale is broadcast)
+  int64_t D;
+  int64_t mod_stride;
+  int64_t nslots;  // G + ngroups - 1
+  int* nonfinite;
+  int nvec;
+  int row_bytes;
+  int nstages;
+  int G;
+};
+
+// Row partition shared by stage 1 and stage 2.
+__host__ __device__ __forceinline__ int64_t part_begin(int64_t k, int64_t N, int64_t G) {
+  return k * N / G;
+}
+// Largest k with part_begin(k) <= row.
+__host__ __device__ __forceinline__ int64_t part_owner(int64_t row, int64_t N, int64_t G) {
+  return ((row + 1) * G - 1) / N;
+}
+
+// Stage schedule walker: stages of at most R rows, never crossing a group boundary.
+struct StageWalker {
+  int64_t row, r1, gend, grp, S;
+  __device__ __forceinline__ void init(int64_t r0, int64_t r1_, int64_t S_) {
+    row = r0;
+    r1 = r1_;
+    S = S_;
+    grp = r0 / S_;
+    gend = (grp + 1) * S_;
+  }
+  __device__ __forceinline__ bool done() const { return row >= r1; }
+  // Rows of the next stage (call only when !done()); advances past it.
+  __device__ __forceinline__ int next(int R, int64_t& start, int64_t& g) {
+    if (row >= gend) {
+      ++grp;
+      gend += S;
+    }
+    const int64_t lim = gend < r1 ? gend : r1;
+    const int64_t left = lim - row;
+    const int n = left < R ? static_cast<int>(left) : R;
+    start = row;
+    g = grp;
+    row += n;
+    return n;
+  }
+};
+
+// =====================================================================================
+// Forward, TMA ring path.  blockDim = nc consumers (multiple of 32) + 1 producer warp.
+// =====================================================================================
+template <typename T, int V, int R>
+__global__ void __launch_bounds__(512) adaln_fwd_tma(const FwdParams p) {
+  using CT = typename Traits<T>::CT;
+  constexpr int EPV = Traits<T>::EPV;
+  extern __shared__ __align__(128) uint8_t smem[];
+
+  const int nc = blockDim.x - 32;
+  const int ncw = nc >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NS = p.nstages;
+  const int RB = p.row_bytes;
+  const int stage_bytes = R * RB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(NS) * stage_bytes);
+  uint64_t* empty = full + NS;
+  CT* red = reinterpret_cast<CT*>(empty + NS);  // [2][ncw][R][2] : (warp mean, warp M2)
+  CT* wcnt = red + 2 * ncw * R * 2;             // [ncw] elements per warp
+
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+
+  uint32_t vmask = 0;
+  int nown = 0;
+  if (tid < nc) {
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+      if (tid + j * nc < p.nvec) {
+        vmask |= 1u << j;
+        ++nown;
+      }
+    const CT nw = warp_sum(static_cast<CT>(nown * EPV));
+    if (lane == 0) wcnt[warp] = nw;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ncw);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == ncw) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const uint8_t* xb = static_cast<const uint8_t*>(p.x);
+      StageWalker w;
+      w.init(r0, r1, p.S_grp);
+      int s = 0;
+      uint32_t f = 0;
+      while (!w.done()) {
+        int64_t start, g;
+        const int rows = w.next(R, start, g);
+        if (f > 0) mbar_wait(&empty[s], (f - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows * RB));
+        uint8_t* dst = smem + static_cast<size_t>(s) * stage_bytes;
+        for (int rr = 0; rr < rows; ++rr)
+          bulk_g2s(dst + rr * RB, xb + (start + rr) * RB, RB, &full[s], pol);
+        if (++s == NS) {
+          s = 0;
+          ++f;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const CT n_t = static_cast<CT>(nown * EPV);
+  const CT inv_nt = nown ? CT(1) / n_t : CT(0);
+  const CT inv_nw = CT(1) / wcnt[warp];
+  const CT invD = CT(1) / static_cast<CT>(p.D);
+  const CT eps = static_cast<CT>(p.eps);
+  bool nf = false;
+
+  CT s1[V][EPV], sh[V][EPV];
+  int64_t cur_g = -1;
+
+  StageWalker w;
+  w.init(r0, r1, p.S_grp);
+  int s = 0;
+  uint32_t ph = 0;
+  int it = 0;
+  while (!w.done()) {
+    int64_t rb, g;
+    const int rows = w.next(R, rb, g);
+    if (g != cur_g) {  // uniform: reload (1+scale), shift of the owned columns
+      cur_g = g;
+      const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
+      const uint8_t* sf = static_cast<const uint8_t*>(p.shift) + g * p.mod_stride * sizeof(T);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if (vmask >> j & 1) {
+          const size_t off = static_cast<size_t>(tid + j * nc) * 16;
+          unpack<T>(__ldg(reinterpret_cast<const uint4*>(sc + off)), s1[j]);
+          unpack<T>(__ldg(reinterpret_cast<const uint4*>(sf + off)), sh[j]);
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) {
+            nf |= !(finite_ct(s1[j][e]) && finite_ct(sh[j][e]));
+            s1[j][e] += CT(1);
+          }
+        }
+      }
+    }
+    mbar_wait(&full[s], ph);
+    const uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
+    CT* rd = red + (it & 1) * (ncw * R * 2);
+
+    // phase 1: per-row statistics of the owned elements, merged within the warp
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (rr < rows) {
+        CT v[V][EPV];
+        CT sum = CT(0);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if (vmask >> j & 1) {
+            unpack<T>(ld_shared_v4(st + rr * RB + (tid + j * nc) * 16), v[j]);
+#pragma unroll
+            for (int e = 0; e < EPV; ++e) sum += v[j][e];
+          }
+        }
+        const CT mt = sum * inv_nt;
+        CT m2 = CT(0);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if (vmask >> j & 1) {
+#pragma unroll
+            for (int e = 0; e < EPV; ++e) {
+              const CT d = v[j][e] - mt;
+              m2 = fma(d, d, m2);
+            }
+          }
+        }
+        const CT mw = warp_sum(sum) * inv_nw;
+        const CT dm = mt - mw;
+        const CT q = warp_sum(fma(n_t * dm, dm, m2));
+        if (lane == 0) {
+          rd[(warp * R + rr) * 2 + 0] = mw;
+          rd[(warp * R + rr) * 2 + 1] = q;
+        }
+      }
+    }
+    named_bar_sync(1, nc);
+
+    // phase 2: merge warps (fixed order), normalise, modulate, store
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (rr < rows) {
+        const int64_t row = rb + rr;
+        CT mean = CT(0);
+        for (int q = 0; q < ncw; ++q) mean = fma(wcnt[q], rd[(q * R + rr) * 2], mean);
+        mean *= invD;
+        CT m2 = CT(0);
+        for (int q = 0; q < ncw; ++q) {
+          const CT d = rd[(q * R + rr) * 2] - mean;
+          m2 += fma(wcnt[q] * d, d, rd[(q * R + rr) * 2 + 1]);
+        }
+        const CT rs = CT(1) / sqrt(m2 * invD + eps);
+        uint8_t* yrow = static_cast<uint8_t*>(p.y) + row * RB;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if (vmask >> j & 1) {
+            CT v[EPV];
+            unpack<T>(ld_shared_v4(st + rr * RB + (tid + j * nc) * 16), v);
+#pragma unroll
+            for (int e = 0; e < EPV; ++e) v[e] = fma((v[e] - mean) * rs, s1[j][e], sh[j][e]);
+            st_global_cs(yrow + (tid + j * nc) * 16, pack<T>(v));
+          }
+        }
+        if (tid == 0) {
+          static_cast<CT*>(p.mean)[row] = mean;
+          static_cast<CT*>(p.rstd)[row] = rs;
+          nf |= !(finite_ct(mean) && finite_ct(m2));
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == NS) {
+      s = 0;
+      ph ^= 1;
+    }
+    ++it;
+  }
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+// =====================================================================================
+// Backward stage 1, TMA ring path.  Stage layout: [x: R rows][dy: R rows].
+// =====================================================================================
+template <typename T, int V, int R>
+__global__ void __launch_bounds__(512) adaln_bwd_tma(const BwdParams p) {
+  using CT = typename Traits<T>::CT;
+  constexpr int EPV = Traits<T>::EPV;
+  extern __shared__ __align__(128) uint8_t smem[];
+
+  const int nc = blockDim.x - 32;
+  const int ncw = nc >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NS = p.nstages;
+  const int RB = p.row_bytes;
+  const int stage_bytes = 2 * R * RB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(NS) * stage_bytes);
+  uint64_t* empty = full + NS;
+  CT* red = reinterpret_cast<CT*>(empty + NS);  // [2][ncw][R][2] : (sum g, sum g*xhat)
+
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ncw);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == ncw) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const uint8_t* xb = static_cast<const uint8_t*>(p.x);
+      const uint8_t* db = static_cast<const uint8_t*>(p.dy);
+      StageWalker w;
+      w.init(r0, r1, p.S_grp);
+      int s = 0;
+      uint32_t f = 0;
+      while (!w.done()) {
+        int64_t start, g;
+        const int rows = w.next(R, start, g);
+        if (f > 0) mbar_wait(&empty[s], (f - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(2 * rows * RB));
+        uint8_t* dst = smem + static_cast<size_t>(s) * stage_bytes;
+        for (int rr = 0; rr < rows; ++rr) {
+          bulk_g2s(dst + rr * RB, xb + (start + rr) * RB, RB, &full[s], pol);
+          bulk_g2s(dst + (R + rr) * RB, db + (start + rr) * RB, RB, &full[s], pol);
+        }
+        if (++s == NS) {
+          s = 0;
+          ++f;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  uint32_t vmask = 0;
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+    if (tid + j * nc < p.nvec) vmask |= 1u << j;
+  const CT invD = CT(1) / static_cast<CT>(p.D);
+  const CT* mean_p = static_cast<const CT*>(p.mean);
+  const CT* rstd_p = static_cast<const CT*>(p.rstd);
+  CT* ws_sc = static_cast<CT*>(p.ws);
+  CT* ws_sh = ws_sc + p.nslots * p.D;
+  bool nf = false;
+
+  CT s1[V][EPV], acc_sc[V][EPV], acc_sh[V][EPV];
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) acc_sc[j][e] = acc_sh[j][e] = CT(0);
+  int64_t cur_g = -1;
+
+  auto flush = [&](int64_t g) {
+    const int64_t slot = k + g;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (vmask >> j & 1) {
+        const int64_t col = static_cast<int64_t>(tid + j * nc) * EPV;
+        CT* a = ws_sc + slot * p.D + col;
+        CT* b = ws_sh + slot * p.D + col;
+#pragma unroll
+        for (int e = 0; e < EPV; e += 16 / sizeof(CT)) {
+          if constexpr (sizeof(CT) == 4) {
+            *reinterpret_cast<float4*>(a + e) =
+                make_float4(acc_sc[j][e], acc_sc[j][e + 1], acc_sc[j][e + 2], acc_sc[j][e + 3]);
+            *reinterpret_cast<float4*>(b + e) =
+                make_float4(acc_sh[j][e], acc_sh[j][e + 1], acc_sh[j][e + 2], acc_sh[j][e + 3]);
+          } else {
+            *reinterpret_cast<double2*>(a + e) = make_double2(acc_sc[j][e], acc_sc[j][e + 1]);
+            *reinterpret_cast<double2*>(b + e) = make_double2(acc_sh[j][e], acc_sh[j][e + 1]);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) acc_sc[j][e] = acc_sh[j][e] = CT(0);
+      }
+    }
+  };
+
+  StageWalker w;
+  w.init(r0, r1, p.S_grp);
+  int s = 0;
+  uint32_t ph = 0;
+  int it = 0;
+
+  // statistics of the current stage's rows (prefetched one stage ahead)
+  StageWalker wp = w;
+  CT mcur[R], rcur[R];
+  {
+    int64_t st0, g0;
+    const int n0 = wp.done() ? 0 : wp.next(R, st0, g0);
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      mcur[rr] = rr < n0 ? mean_p[st0 + rr] : CT(0);
+      rcur[rr] = rr < n0 ? rstd_p[st0 + rr] : CT(0);
+    }
+  }
+
+  while (!w.done()) {
+    int64_t rb, g;
+    const int rows = w.next(R, rb, g);
+    CT mnext[R], rnext[R];
+    {
+      int64_t st1 = 0, g1;
+      const int n1 = wp.done() ? 0 : wp.next(R, st1, g1);
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        mnext[rr] = rr < n1 ? mean_p[st1 + rr] : CT(0);
+        rnext[rr] = rr < n1 ? rstd_p[st1 + rr] : CT(0);
+      }
+    }
+    if (g != cur_g) {
+      if (cur_g >= 0) flush(cur_g);
+      cur_g = g;
+      const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if (vmask >> j & 1) {
+          unpack<T>(__ldg(reinterpret_cast<const uint4*>(sc + static_cast<size_t>(tid + j * nc) * 16)),
+                    s1[j]);
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) s1[j][e] += CT(1);
+        }
+      }
+    }
+    mbar_wait(&full[s], ph);
+    const uint8_t* stx = smem + static_cast<size_t>(s) * stage_bytes;
+    const uint8_t* std_ = stx + R * RB;
+    CT* rd = red + (it & 1) * (ncw * R * 2);
+
+    // phase 1: row sums of g and g*xhat; column accumulators of dy and dy*xhat
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (rr < rows) {
+        const CT m = mcur[rr], r = rcur[rr];
+        CT sg = CT(0), sgx = CT(0);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if (vmask >> j & 1) {
+            CT xv[EPV], dv[EPV];
+            unpack<T>(ld_shared_v4(stx + rr * RB + (tid + j * nc) * 16), xv);
+            unpack<T>(ld_shared_v4(std_ + rr * RB + (tid + j * nc) * 16), dv);
+#pragma unroll
+            for (int e = 0; e < EPV; ++e) {
+              const CT xh = (xv[e] - m) * r;
+              const CT gg = dv[e] * s1[j][e];
+              sg += gg;
+              sgx = fma(gg, xh, sgx);
+              acc_sh[j][e] += dv[e];
+              acc_sc[j][e] = fma(dv[e], xh, acc_sc[j][e]);
+            }
+          }
+        }
+        sg = warp_sum(sg);
+        sgx = warp_sum(sgx);
+        if (lane == 0) {
+          rd[(warp * R + rr) * 2 + 0] = sg;
+          rd[(warp * R + rr) * 2 + 1] = sgx;
+        }
+      }
+    }
+    named_bar_sync(1, nc);
+
+    // phase 2: dx = rstd * (g - mean(g) - xhat * mean(g*xhat))
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (rr < rows) {
+        const int64_t row = rb + rr;
+        const CT m = mcur[rr], r = rcur[rr];
+        CT tg = CT(0), tgx = CT(0);
+        for (int q = 0; q < ncw; ++q) {
+          tg += rd[(q * R + rr) * 2 + 0];
+          tgx += rd[(q * R + rr) * 2 + 1];
+        }
+        const CT mg = tg * invD, mgx = tgx * invD;
+        uint8_t* dxrow = static_cast<uint8_t*>(p.dx) + row * RB;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if (vmask >> j & 1) {
+            CT xv[EPV], dv[EPV];
+            unpack<T>(ld_shared_v4(stx + rr * RB + (tid + j * nc) * 16), xv);
+            unpack<T>(ld_shared_v4(std_ + rr * RB + (tid + j * nc) * 16), dv);
+#pragma unroll
+            for (int e = 0; e < EPV; ++e) {
+              const CT xh = (xv[e] - m) * r;
+              const CT gg = dv[e] * s1[j][e];
+              xv[e] = r * fma(-xh, mgx, gg - mg);
+            }
+            st_global_cs(dxrow + (tid + j * nc) * 16, pack<T>(xv));
+          }
+        }
+        if (tid == 0) nf |= !(finite_ct(tg) && finite_ct(tgx));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == NS) {
+      s = 0;
+      ph ^= 1;
+    }
+    ++it;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      mcur[rr] = mnext[rr];
+      rcur[rr] = rnext[rr];
+    }
+  }
+  if (cur_g >= 0) flush(cur_g);
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+// =====================================================================================
+// Backward stage 2: dscale/dshift[g, d] = sum over the CTAs covering group g, ascending.
+// grid = (ceil(D/32), ngroups), block = 256 (8 slot lanes x 32 columns).
+// =====================================================================================
+template <typename CT>
+__global__ void __launch_bounds__(256) adaln_bwd_reduce(const CT* __restrict__ ws,
+                                                        CT* __restrict__ dscale,
+                                                        CT* __restrict__ dshift, int64_t N,
+                                                        int64_t S_grp, int64_t D, int64_t G,
+                                                        int64_t nslots) {
+  __shared__ double part[2][8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t g = blockIdx.y;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  const int64_t first_row = g * S_grp;
+  const int64_t last_row = ((g + 1) * S_grp < N ? (g + 1) * S_grp : N) - 1;
+  const int64_t kf = part_owner(first_row, N, G), kl = part_owner(last_row, N, G);
+  double a = 0.0, b = 0.0;
+  if (col < D) {
+    const CT* sc = ws + col;
+    const CT* sh = ws + nslots * D + col;
+#pragma unroll 4
+    for (int64_t kk = kf + w; kk <= kl; kk += 8) {
+      a += static_cast<double>(sc[(kk + g) * D]);
+      b += static_cast<double>(sh[(kk + g) * D]);
+    }
+  }
+  part[0][w][lane] = a;
+  part[1][w][lane] = b;
+  __syncthreads();
+  if (w == 0 && col < D) {
+    double ta = 0.0, tb = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      ta += part[0][q][lane];
+      tb += part[1][q][lane];
+    }
+    dscale[g * D + col] = static_cast<CT>(ta);
+    dshift[g * D + col] = static_cast<CT>(tb);
+  }
+}
+
+// =====================================================================================
+// Generic (any D, any alignment) kernels.  Correctness path for shapes the vector/TMA path
+// cannot take (D*sizeof(T) not a multiple of 16, unaligned views, very wide rows).
+// =====================================================================================
+template <typename T>
+__global__ void __launch_bounds__(256) adaln_fwd_generic(const FwdParams p) {
+  using CT = typename Traits<T>::CT;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const T* x = static_cast<const T*>(p.x);
+  const T* sc = static_cast<const T*>(p.scale);
+  const T* sf = static_cast<const T*>(p.shift);
+  T* y = static_cast<T*>(p.y);
+  const CT eps = static_cast<CT>(p.eps);
+  bool nf = false;
+  for (int64_t row = wid; row < p.N; row += nw) {
+    const T* xr = x + row * p.D;
+    const int64_t g = row / p.S_grp;
+    CT sum = CT(0);
+    for (int64_t j = lane; j < p.D; j += 32) sum += to_ct(xr[j]);
+    const CT mean = warp_sum(sum) / static_cast<CT>(p.D);
+    CT m2 = CT(0);
+    for (int64_t j = lane; j < p.D; j += 32) {
+      const CT d = to_ct(xr[j]) - mean;
+      m2 = fma(d, d, m2);
+    }
+    m2 = warp_sum(m2);
+    const CT rs = CT(1) / sqrt(m2 / static_cast<CT>(p.D) + eps);
+    for (int64_t j = lane; j < p.D; j += 32) {
+      const CT a = to_ct(sc[g * p.mod_stride + j]), b = to_ct(sf[g * p.mod_stride + j]);
+      nf |= !(finite_ct(a) && finite_ct(b));
+      y[row * p.D + j] = from_ct<T>(fma((to_ct(xr[j]) - mean) * rs, CT(1) + a, b));
+    }
+    if (lane == 0) {
+      static_cast<CT*>(p.mean)[row] = mean;
+      static_cast<CT*>(p.rstd)[row] = rs;
+      nf |= !(finite_ct(mean) && finite_ct(m2));
+    }
+  }
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) adaln_bwd_generic(const BwdParams p) {
+  using CT = typename Traits<T>::CT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+  const T* x = static_cast<const T*>(p.x);
+  const T* dy = static_cast<const T*>(p.dy);
+  const T* sc = static_cast<const T*>(p.scale);
+  const CT* mean_p = static_cast<const CT*>(p.mean);
+  const CT* rstd_p = static_cast<const CT*>(p.rstd);
+  T* dx = static_cast<T*>(p.dx);
+  const CT invD = CT(1) / static_cast<CT>(p.D);
+  bool nf = false;
+  // dx: one warp per row
+  for (int64_t row = r0 + warp; row < r1; row += nwarp) {
+    const int64_t g = row / p.S_grp;
+    const CT m = mean_p[row], r = rstd_p[row];
+    CT sg = CT(0), sgx = CT(0);
+    for (int64_t j = lane; j < p.D; j += 32) {
+      const CT xh = (to_ct(x[row * p.D + j]) - m) * r;
+      const CT gg = to_ct(dy[row * p.D + j]) * (CT(1) + to_ct(sc[g * p.mod_stride + j]));
+      sg += gg;
+      sgx = fma(gg, xh, sgx);
+    }
+    sg = warp_sum(sg);
+    sgx = warp_sum(sgx);
+    const CT mg = sg * invD, mgx = sgx * invD;
+    for (int64_t j = lane; j < p.D; j += 32) {
+      const CT xh = (to_ct(x[row * p.D + j]) - m) * r;
+      const CT gg = to_ct(dy[row * p.D + j]) * (CT(1) + to_ct(sc[g * p.mod_stride + j]));
+      dx[row * p.D + j] = from_ct<T>(r * fma(-xh, mgx, gg - mg));
+    }
+    if (lane == 0) nf |= !(finite_ct(sg) && finite_ct(sgx));
+  }
+  // stage-1 column partials: thread per column, rows ascending
+  CT* ws_sc = static_cast<CT*>(p.ws);
+  CT* ws_sh = ws_sc + p.nslots * p.D;
+  for (int64_t col = threadIdx.x; col < p.D; col += blockDim.x) {
+    int64_t g = r0 / p.S_grp;
+    int64_t gend = (g + 1) * p.S_grp;
+    CT a = CT(0), b = CT(0);
+    for (int64_t row = r0; row < r1; ++row) {
+      if (row >= gend) {
+        ws_sc[(k + g) * p.D + col] = a;
+        ws_sh[(k + g) * p.D + col] = b;
+        a = b = CT(0);
+        ++g;
+        gend += p.S_grp;
+      }
+      const CT d = to_ct(dy[row * p.D + col]);
+      const CT xh = (to_ct(x[row * p.D + col]) - mean_p[row]) * rstd_p[row];
+      b += d;
+      a = fma(d, xh, a);
+    }
+    ws_sc[(k + g) * p.D + col] = a;
+    ws_sh[(k + g) * p.D + col] = b;
+  }
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+}  // namespace al

@@ -1,0 +1,138 @@
+// dtype.cuh -- element traits for the AdaLN kernels: 16-byte vector pack/unpack for
+// bf16 / fp16 / fp32 (computed in fp32) and fp64 (computed in fp64).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+
+namespace al {
+
+template <typename T>
+struct Traits;
+
+template <>
+struct Traits<float> {
+  using CT = float;  // compute / statistics / partial type
+  static constexpr int EPV = 4;  // elements per 16-byte vector
+};
+template <>
+struct Traits<__nv_bfloat16> {
+  using CT = float;
+  static constexpr int EPV = 8;
+};
+template <>
+struct Traits<__half> {
+  using CT = float;
+  static constexpr int EPV = 8;
+};
+template <>
+struct Traits<double> {
+  using CT = double;
+  static constexpr int EPV = 2;
+};
+
+// ---- scalar conversions (generic path) --------------------------------------------------------
+__device__ __forceinline__ float to_ct(float v) { return v; }
+__device__ __forceinline__ double to_ct(double v) { return v; }
+__device__ __forceinline__ float to_ct(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float to_ct(__half v) { return __half2float(v); }
+
+template <typename T>
+__device__ __forceinline__ T from_ct(typename Traits<T>::CT v);
+template <>
+__device__ __forceinline__ float from_ct<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ double from_ct<double>(double v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_ct<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+template <>
+__device__ __forceinline__ __half from_ct<__half>(float v) { return __float2half_rn(v); }
+
+// ---- 16-byte vector unpack / pack ---------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void unpack(const uint4& v, typename Traits<T>::CT* out);
+
+template <>
+__device__ __forceinline__ void unpack<float>(const uint4& v, float* o) {
+  o[0] = __uint_as_float(v.x);
+  o[1] = __uint_as_float(v.y);
+  o[2] = __uint_as_float(v.z);
+  o[3] = __uint_as_float(v.w);
+}
+template <>
+__device__ __forceinline__ void unpack<double>(const uint4& v, double* o) {
+  o[0] = __hiloint2double(static_cast<int>(v.y), static_cast<int>(v.x));
+  o[1] = __hiloint2double(static_cast<int>(v.w), static_cast<int>(v.z));
+}
+template <>
+__device__ __forceinline__ void unpack<__nv_bfloat16>(const uint4& v, float* o) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o[2 * i] = __uint_as_float(w[i] << 16);
+    o[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+template <>
+__device__ __forceinline__ void unpack<__half>(const uint4& v, float* o) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+    float2 f = __half22float2(h);
+    o[2 * i] = f.x;
+    o[2 * i + 1] = f.y;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ uint4 pack(const typename Traits<T>::CT* in);
+
+template <>
+__device__ __forceinline__ uint4 pack<float>(const float* i) {
+  return make_uint4(__float_as_uint(i[0]), __float_as_uint(i[1]), __float_as_uint(i[2]),
+                    __float_as_uint(i[3]));
+}
+template <>
+__device__ __forceinline__ uint4 pack<double>(const double* i) {
+  return make_uint4(static_cast<uint32_t>(__double2loint(i[0])),
+                    static_cast<uint32_t>(__double2hiint(i[0])),
+                    static_cast<uint32_t>(__double2loint(i[1])),
+                    static_cast<uint32_t>(__double2hiint(i[1])));
+}
+template <>
+__device__ __forceinline__ uint4 pack<__nv_bfloat16>(const float* i) {
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(i[2 * k], i[2 * k + 1]);
+    w[k] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+template <>
+__device__ __forceinline__ uint4 pack<__half>(const float* i) {
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    __half2 h = __floats2half2_rn(i[2 * k], i[2 * k + 1]);
+    w[k] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <typename CT>
+__device__ __forceinline__ bool finite_ct(CT v) {
+  return isfinite(v);
+}
+
+template <typename CT>
+__device__ __forceinline__ CT warp_sum(CT v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace al

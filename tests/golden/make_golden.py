@@ -1,0 +1,211 @@
+"""Generate the golden fixtures by running the REFERENCE implementation (this container only).
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Imports the reference package in place from /root/reference/pkg/src (read-only; numba backend,
+as shipped) and records its outputs on fixed inputs:
+
+* adaln_golden.npz   -- adaln_forward / adaln_backward_naive / adaln_backward_dtile (f64 and
+                        fp32-accumulator variants) on the reference test suite's cases
+                        (test_adaln.py rand_case seeds, hand example, degenerate cases) plus a
+                        Wan-width (D=5120) bf16-rounded case and a +50-offset case.
+* sampler_golden.json -- dual_constraint_batch / equal_token_batch / emit_plan results,
+                        sample_assignments draws as consumed by run_policy (choice + normal per
+                        step), per-step compute_cv, and run_experiment summaries at 2/4/8/16 ranks.
+
+The fixtures are committed; /root/reference does not exist on the GPU box.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+OUT = Path(__file__).resolve().parent
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+sys.path.insert(0, REF_SRC)
+
+from adaptiveload import adaln  # noqa: E402
+from adaptiveload.cluster_sim import (  # noqa: E402
+    ClusterConfig, compute_cv, default_catalog, default_dual_constraint, default_token_budget,
+    run_experiment, run_policy)
+from adaptiveload.scheduler import (  # noqa: E402
+    DualConstraint, TokenBudget, dual_constraint_batch, emit_plan, equal_token_batch)
+from adaptiveload.shapes import LatentGeometry, MediaShape, build_catalog, sequence_length  # noqa: E402
+
+assert adaln.BACKEND == "numba", adaln.BACKEND
+
+
+def rand_case(n, d, seed=0):  # test_adaln.py:20-27
+    rng = np.random.default_rng(seed)
+    return (rng.standard_normal((n, d)), 0.5 * rng.standard_normal(d),
+            0.5 * rng.standard_normal(d), rng.standard_normal((n, d)))
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even to bfloat16, returned as float64 (what the GPU sees, upcast)."""
+    f = np.asarray(a, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def adaln_cases():
+    cases = {}
+    x = np.array([[1.0, 2.0], [3.0, 5.0]])
+    cases["hand"] = (x, np.array([0.5, -0.5]), np.array([1.0, 2.0]),
+                     np.array([[0.3, -1.2], [0.7, 2.0]]), 1e-6)
+    for (n, d, seed) in [(5, 8, 0), (64, 16, 2), (32, 8, 4), (64, 32, 3), (128, 32, 8),
+                         (7, 4, 0), (1, 16, 0), (8, 16, 1), (4, 6, 0), (512, 64, 5)]:
+        xx, sc, sh, dy = rand_case(n, d, seed)
+        cases[f"rand_{n}x{d}_s{seed}"] = (xx, sc, sh, dy, 1e-6)
+    cases["d1"] = (np.array([[3.0], [5.0], [-1.0]]), np.array([0.7]), np.array([2.0]),
+                   np.ones((3, 1)), 1e-6)
+    rng = np.random.default_rng(10)
+    x6 = rng.standard_normal((6, 5))
+    cases["scale_minus1"] = (x6, -np.ones(5), np.zeros(5), rng.standard_normal((6, 5)), 1e-6)
+    rng = np.random.default_rng(2605)
+    cases["wan_bf16_3x5120"] = (bf16_round(rng.standard_normal((3, 5120))),
+                                bf16_round(0.1 * rng.standard_normal(5120)),
+                                bf16_round(0.1 * rng.standard_normal(5120)),
+                                bf16_round(rng.standard_normal((3, 5120))), 1e-6)
+    rng = np.random.default_rng(50)
+    cases["offset50_96x320"] = (50.0 + rng.standard_normal((96, 320)),
+                                0.3 * rng.standard_normal(320), 0.3 * rng.standard_normal(320),
+                                rng.standard_normal((96, 320)), 1e-6)
+    return cases
+
+
+TILES = [(1, 1), (3, 7), (8, 128), (64, 1), (64, 4096), (13, 999)]
+
+
+def make_adaln():
+    arrays = {}
+    names = []
+    for name, (x, sc, sh, dy, eps) in adaln_cases().items():
+        n, d = x.shape
+        out = adaln.adaln_forward(x, sc, sh, eps)
+        g = adaln.adaln_backward_naive(dy, x, sc, out.mu, out.rstd)
+        p = f"{name}/"
+        arrays.update({p + "x": x, p + "scale": sc, p + "shift": sh, p + "dy": dy,
+                       p + "eps": np.array(eps), p + "y": out.y, p + "mu": out.mu,
+                       p + "rstd": out.rstd, p + "dx": g.dx, p + "dscale": g.dscale,
+                       p + "dshift": g.dshift})
+        tiles = sorted({(min(a, d), min(b, n)) for a, b in TILES})
+        arrays[p + "tiles"] = np.array(tiles, dtype=np.int64)
+        for (dt, nt) in tiles:
+            for acc in (0, 1):
+                gt = adaln.adaln_backward_dtile(dy, x, sc, out.mu, out.rstd,
+                                                adaln.TileConfig(dt, nt), fp32_accum=bool(acc))
+                q = f"{p}dtile_{dt}_{nt}_{acc}/"
+                arrays[q + "dscale"] = gt.dscale
+                arrays[q + "dshift"] = gt.dshift
+                if acc == 0 and (dt, nt) == tiles[0]:
+                    arrays[p + "dtile_dx"] = gt.dx
+        names.append(name)
+    arrays["__cases__"] = np.array(names)
+    np.savez_compressed(OUT / "adaln_golden.npz", **arrays)
+
+
+def wan_catalog_shapes():
+    """Wan-2.1 lambda=4 shapes: 480x832 and 720x1280 stills and 17..81-frame videos."""
+    shapes = [(MediaShape(1, 480, 832), 40), (MediaShape(1, 720, 1280), 20)]
+    for f, c in [(17, 24), (33, 16), (49, 10), (65, 6), (81, 4)]:
+        shapes.append((MediaShape(f, 480, 832), c))
+    for f, c in [(17, 8), (33, 5), (49, 3), (81, 2)]:
+        shapes.append((MediaShape(f, 720, 1280), c))
+    return shapes
+
+
+def plan_json(plan):
+    return [{"seq_len": e.bucket.seq_len, "batch": e.batch_size,
+             "binding": None if e.binding is None else e.binding.value} for e in plan.entries]
+
+
+def make_sampler():
+    out = {}
+    rng = np.random.default_rng(11)
+    grid = [round(1.6 + 0.05 * i, 10) for i in range(17)]
+    cases = []
+    for _ in range(2000):
+        s = int(rng.integers(100, 100_000))
+        c = (float(rng.integers(1_000, 1_000_000)), float(rng.uniform(1e4, 1e12)),
+             float(rng.choice(grid)))
+        b, binding = dual_constraint_batch(s, DualConstraint(*c))
+        cases.append([s, *c, b, binding.value])
+    for s, c in [(10000, (100000, 2e9, 2)), (10**9, (1e6, 1e12, 2)), (48000, (1e6, 1.2e10, 2)),
+                 (10, (100, 1000, 2)), (1, (48000, 48000, 1.0)), (52801, (48000, 48000, 1.0))]:
+        b, binding = dual_constraint_batch(s, DualConstraint(*map(float, c)))
+        cases.append([s, *map(float, c), b, binding.value])
+    out["dual_constraint_batch"] = cases
+    out["equal_token_batch"] = [[s, t, equal_token_batch(s, TokenBudget(t))]
+                                for s, t in [(1600, 48000), (48000, 48000), (100000, 48000),
+                                             (1, 7), (7, 7), (480000, 480000), (1560, 480000)]]
+
+    catalogs = {}
+    cat, w = default_catalog()
+    catalogs["default"] = (cat, w, LatentGeometry(), default_token_budget(),
+                           default_dual_constraint())
+    geom4 = LatentGeometry(temporal_factor=4)
+    wcat = build_catalog(wan_catalog_shapes(), geom4)
+    tot = sum(b.sample_count for b in wcat)
+    catalogs["wan_l4"] = (wcat, [b.sample_count / tot for b in wcat], geom4,
+                          TokenBudget(480_000), DualConstraint(480_000, 3e9, 2.0))
+    out["catalogs"] = {}
+    for cname, (cat, w, geom, tb, dc) in catalogs.items():
+        plan_a = emit_plan(cat, tb)
+        plan_b = emit_plan(cat, dc)
+        entry = {
+            "geometry": [geom.temporal_factor, geom.width_factor, geom.height_factor,
+                         geom.text_tokens],
+            "shapes": [[b.shape.frames, b.shape.height, b.shape.width, b.sample_count]
+                       for b in cat],
+            "seq_len": [b.seq_len for b in cat],
+            "weights": list(w),
+            "token_budget": tb.budget,
+            "dual": [dc.m_mem, dc.m_comp, dc.p],
+            "plan_equal_token": plan_json(plan_a),
+            "plan_dual": plan_json(plan_b),
+            "draws": {},
+        }
+        index = {b.shape: i for i, b in enumerate(cat)}
+        for policy, plan in (("equal_token", plan_a), ("dual", plan_b)):
+            for nw in (2, 8):
+                for seed in (0, 42):
+                    cfg = ClusterConfig(num_workers=nw, steps=40, seed=seed)
+                    series, recs, _ = run_policy(cat, w, plan, cfg, np.random.default_rng(seed),
+                                                 geom, collect_records=True)
+                    idx = [[index[wk.bucket.shape] for wk in r.per_worker] for r in recs]
+                    bs = [[wk.batch_size for wk in r.per_worker] for r in recs]
+                    entry["draws"][f"{policy}/n{nw}/seed{seed}"] = {
+                        "idx": idx, "batch": bs,
+                        "compute_cv": [float(v) for v in series.compute_cv],
+                        "compute_cv_range": [float(v) for v in series.compute_cv_range],
+                    }
+        entry["experiments"] = {}
+        for nw in (2, 4, 8, 16):
+            res = run_experiment(cat, w, plan_a, plan_b,
+                                 ClusterConfig(num_workers=nw, steps=500, seed=42), geom)
+            entry["experiments"][str(nw)] = res.summary
+        out["catalogs"][cname] = entry
+
+    shapes = [(1, 640, 640), (17, 640, 640), (233, 640, 640), (257, 640, 640), (1, 480, 832),
+              (81, 480, 832), (81, 720, 1280), (1, 16, 16)]
+    out["sequence_length"] = {
+        "lambda8": [[*s, sequence_length(MediaShape(*s), LatentGeometry())]
+                    for s in shapes if (s[0] - 1) % 8 == 0],
+        "lambda4": [[*s, sequence_length(MediaShape(*s), geom4)] for s in shapes],
+    }
+    (OUT / "sampler_golden.json").write_text(json.dumps(out, indent=1, sort_keys=True))
+
+
+if __name__ == "__main__":
+    make_adaln()
+    make_sampler()
+    print("wrote", sorted(p.name for p in OUT.iterdir()))
