@@ -108,13 +108,18 @@ AL_API int al_adaln_backward(const void* dy, const void* x, const void* scale,
 /*
  * Tuning overrides for benchmarking sweeps (0 = automatic).  kernel: 0 = forward, 1 = backward.
  * vecs_per_thread in {1,2,4}; rows_per_stage in {1,2,4}; smem_budget in bytes per CTA;
- * force_generic = 1 routes through the generic (any-shape) kernels.  Process-global.
+ * force_generic = 1 routes through the generic (any-shape) kernels.  variant selects a
+ * code-generation variant of the forward rows kernel (0 auto, 1 re-expand packed rows per pass,
+ * 2 let the compiler keep the row unpacked).  Process-global.  For the forward kernel a nonzero
+ * vecs_per_thread / rows_per_stage selects the wide (TMA ring) path.
  */
 AL_API int al_set_tuning(int kernel, int vecs_per_thread, int rows_per_stage, int smem_budget,
-                  int force_generic);
+                         int force_generic, int variant);
 
 /* Describe the launch al_adaln_{forward,backward} would use: writes
- * {path(0 generic,1 tma), grid, threads, vecs_per_thread, rows_per_stage, stages, smem_bytes}. */
+ * {path (0 generic, 1 TMA ring, 2 rows-in-registers), grid, threads, vecs_per_thread (rows
+ * path: 16-byte vectors per lane), rows_per_stage (rows path: 1 if the re-expanding variant),
+ * stages, smem_bytes}. */
 AL_API int al_describe_launch(int kernel, int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
                        int dtype, int64_t n_tile, int64_t out[7]);
 

@@ -45,7 +45,7 @@ _SIGNATURES = {
         [_p, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, ctypes.c_int,
          _i64, _i64, _p, _p],
     ),
-    "al_set_tuning": (ctypes.c_int, [ctypes.c_int] * 5),
+    "al_set_tuning": (ctypes.c_int, [ctypes.c_int] * 6),
     "al_describe_launch": (
         ctypes.c_int,
         [ctypes.c_int, _i64, _i64, _i64, _i64, ctypes.c_int, _i64, ctypes.POINTER(_i64)],
@@ -120,9 +120,9 @@ def ensure_device(device_index: int) -> None:
 
 
 def set_tuning(kernel: int, vecs_per_thread: int = 0, rows_per_stage: int = 0,
-               smem_budget: int = 0, force_generic: bool = False) -> None:
+               smem_budget: int = 0, force_generic: bool = False, variant: int = 0) -> None:
     check(load().al_set_tuning(kernel, vecs_per_thread, rows_per_stage, smem_budget,
-                               int(force_generic)), "al_set_tuning")
+                               int(force_generic), variant), "al_set_tuning")
 
 
 def describe_launch(kernel: int, batch: int, seq: int, dim: int, mod_stride: int, dtype: int,
@@ -132,5 +132,5 @@ def describe_launch(kernel: int, batch: int, seq: int, dim: int, mod_stride: int
           "al_describe_launch")
     keys = ("path", "grid", "threads", "vecs_per_thread", "rows_per_stage", "stages", "smem_bytes")
     d = dict(zip(keys, list(out)))
-    d["path"] = "tma" if d["path"] == 1 else "generic"
+    d["path"] = {0: "generic", 1: "tma", 2: "rows"}[d["path"]]
     return d

@@ -30,14 +30,13 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 // ---------------------------------------------------------------- tuning
 struct Tuning {
-  int V = 0, R = 0, smem_budget = 0, force_generic = 0;
+  int V = 0, R = 0, smem_budget = 0, force_generic = 0, variant = 0;
 };
 Tuning g_tune[2];
 std::mutex g_mu;
 
-constexpr int kMaxThreads = 512;        // __launch_bounds__ of the TMA kernels
 constexpr int kSmemOptin = 227 * 1024;  // sm_100 per-CTA opt-in maximum
-constexpr int kDefaultBudget[2] = {100 * 1024, 100 * 1024};
+constexpr int kDefaultBudget[2] = {100 * 1024, 200 * 1024};
 constexpr int kDefaultR[2] = {2, 2};
 
 // ---------------------------------------------------------------- device info
@@ -70,22 +69,48 @@ int dev_sms(int dev, int* sms) {
 using FwdFn = void (*)(al::FwdParams);
 using BwdFn = void (*)(al::BwdParams);
 
+constexpr int kVpl[] = {1, 2, 3, 4, 6, 8, 12, 16, 20, 24};  // rows-path vectors per lane
+constexpr int kNumVpl = sizeof(kVpl) / sizeof(kVpl[0]);
+constexpr int kMaxVpl = 24;
+
 template <typename T>
 struct Table {
-  FwdFn fwd[3][3];  // [V idx][R idx], V in {1,2,4}, R in {1,2,4}
+  FwdFn rows[kNumVpl];
+  FwdFn rows_rp[kNumVpl];  // REPACK variant
+  FwdFn wide[3][3];  // [V idx][R idx], V in {1,2,4}, R in {1,2,4}
   BwdFn bwd[3][3];
   FwdFn fwd_generic;
   BwdFn bwd_generic;
   Table() {
-    fwd[0][0] = al::adaln_fwd_tma<T, 1, 1>;
-    fwd[0][1] = al::adaln_fwd_tma<T, 1, 2>;
-    fwd[0][2] = al::adaln_fwd_tma<T, 1, 4>;
-    fwd[1][0] = al::adaln_fwd_tma<T, 2, 1>;
-    fwd[1][1] = al::adaln_fwd_tma<T, 2, 2>;
-    fwd[1][2] = al::adaln_fwd_tma<T, 2, 4>;
-    fwd[2][0] = al::adaln_fwd_tma<T, 4, 1>;
-    fwd[2][1] = al::adaln_fwd_tma<T, 4, 2>;
-    fwd[2][2] = al::adaln_fwd_tma<T, 4, 4>;
+    rows[0] = al::adaln_fwd_rows<T, 1, false>;
+    rows_rp[0] = al::adaln_fwd_rows<T, 1, true>;
+    rows[1] = al::adaln_fwd_rows<T, 2, false>;
+    rows_rp[1] = al::adaln_fwd_rows<T, 2, true>;
+    rows[2] = al::adaln_fwd_rows<T, 3, false>;
+    rows_rp[2] = al::adaln_fwd_rows<T, 3, true>;
+    rows[3] = al::adaln_fwd_rows<T, 4, false>;
+    rows_rp[3] = al::adaln_fwd_rows<T, 4, true>;
+    rows[4] = al::adaln_fwd_rows<T, 6, false>;
+    rows_rp[4] = al::adaln_fwd_rows<T, 6, true>;
+    rows[5] = al::adaln_fwd_rows<T, 8, false>;
+    rows_rp[5] = al::adaln_fwd_rows<T, 8, true>;
+    rows[6] = al::adaln_fwd_rows<T, 12, false>;
+    rows_rp[6] = al::adaln_fwd_rows<T, 12, true>;
+    rows[7] = al::adaln_fwd_rows<T, 16, false>;
+    rows_rp[7] = al::adaln_fwd_rows<T, 16, true>;
+    rows[8] = al::adaln_fwd_rows<T, 20, false>;
+    rows_rp[8] = al::adaln_fwd_rows<T, 20, true>;
+    rows[9] = al::adaln_fwd_rows<T, 24, false>;
+    rows_rp[9] = al::adaln_fwd_rows<T, 24, true>;
+    wide[0][0] = al::adaln_fwd_wide<T, 1, 1>;
+    wide[0][1] = al::adaln_fwd_wide<T, 1, 2>;
+    wide[0][2] = al::adaln_fwd_wide<T, 1, 4>;
+    wide[1][0] = al::adaln_fwd_wide<T, 2, 1>;
+    wide[1][1] = al::adaln_fwd_wide<T, 2, 2>;
+    wide[1][2] = al::adaln_fwd_wide<T, 2, 4>;
+    wide[2][0] = al::adaln_fwd_wide<T, 4, 1>;
+    wide[2][1] = al::adaln_fwd_wide<T, 4, 2>;
+    wide[2][2] = al::adaln_fwd_wide<T, 4, 4>;
     bwd[0][0] = al::adaln_bwd_tma<T, 1, 1>;
     bwd[0][1] = al::adaln_bwd_tma<T, 1, 2>;
     bwd[0][2] = al::adaln_bwd_tma<T, 1, 4>;
@@ -118,24 +143,32 @@ int elem_size(int dtype) {
 }
 int ct_size(int dtype) { return dtype == AL_F64 ? 8 : 4; }
 
+template <typename F>
+auto with_table(int dtype, F&& f) {
+  switch (dtype) {
+    case AL_BF16: return f(t_bf16);
+    case AL_F16: return f(t_f16);
+    case AL_F64: return f(t_f64);
+    default: return f(t_f32);
+  }
+}
+
+// path: 1 = TMA ring (wide forward / backward), 2 = rows-in-registers forward
 const void* tma_kernel(int kernel, int dtype, int V, int R) {
   const int a = vidx(V), b = vidx(R);
-  switch (dtype) {
-    case AL_F32: return kernel ? (const void*)t_f32.bwd[a][b] : (const void*)t_f32.fwd[a][b];
-    case AL_BF16: return kernel ? (const void*)t_bf16.bwd[a][b] : (const void*)t_bf16.fwd[a][b];
-    case AL_F16: return kernel ? (const void*)t_f16.bwd[a][b] : (const void*)t_f16.fwd[a][b];
-    case AL_F64: return kernel ? (const void*)t_f64.bwd[a][b] : (const void*)t_f64.fwd[a][b];
-  }
-  return nullptr;
+  return with_table(dtype, [&](const auto& t) {
+    return kernel ? (const void*)t.bwd[a][b] : (const void*)t.wide[a][b];
+  });
+}
+const void* rows_kernel(int dtype, int vi, bool repack) {
+  return with_table(dtype, [&](const auto& t) {
+    return repack ? (const void*)t.rows_rp[vi] : (const void*)t.rows[vi];
+  });
 }
 const void* generic_kernel(int kernel, int dtype) {
-  switch (dtype) {
-    case AL_F32: return kernel ? (const void*)t_f32.bwd_generic : (const void*)t_f32.fwd_generic;
-    case AL_BF16: return kernel ? (const void*)t_bf16.bwd_generic : (const void*)t_bf16.fwd_generic;
-    case AL_F16: return kernel ? (const void*)t_f16.bwd_generic : (const void*)t_f16.fwd_generic;
-    case AL_F64: return kernel ? (const void*)t_f64.bwd_generic : (const void*)t_f64.fwd_generic;
-  }
-  return nullptr;
+  return with_table(dtype, [&](const auto& t) {
+    return kernel ? (const void*)t.bwd_generic : (const void*)t.fwd_generic;
+  });
 }
 const void* reduce_kernel(int dtype) {
   return dtype == AL_F64 ? (const void*)al::adaln_bwd_reduce<double>
@@ -167,7 +200,7 @@ int ensure_attr(const void* fn, int dev) {
 
 // ---------------------------------------------------------------- launch planning
 struct Plan {
-  int path = 0;  // 0 generic, 1 tma
+  int path = 0;  // 0 generic, 1 tma ring, 2 rows-in-registers
   int grid = 0, threads = 0, V = 0, R = 0, NS = 0;
   size_t smem = 0;
   const void* fn = nullptr;
@@ -175,8 +208,55 @@ struct Plan {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// kernel: 0 fwd, 1 bwd.  `ptrs` are the row-tensor / modulation pointers that the vector path
-// reads or writes with 16-byte accesses.
+int occupancy(const Plan& pl, int dev, int* occ) {
+  int rc = ensure_attr(pl.fn, dev);
+  if (rc) return rc;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, pl.fn, pl.threads, pl.smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  return AL_OK;
+}
+
+// TMA-ring plan (wide forward or backward); returns false if the shape does not fit.
+bool ring_plan(int kernel, int64_t nvec, int row_bytes, int cs, const Tuning& tu, Plan* pl) {
+  const int max_threads = kernel ? 384 : 512;  // __launch_bounds__ of the kernels
+  const int vcap = kernel ? 352 : 256;
+  int V = tu.V;
+  if (V == 0) {
+    V = 4;
+    for (int v : {1, 2, 4})
+      if (((nvec + v - 1) / v + 31) / 32 * 32 <= vcap) {
+        V = v;
+        break;
+      }
+  }
+  const int64_t nc = ((nvec + V - 1) / V + 31) / 32 * 32;
+  if (nc + 32 > max_threads) return false;
+  const int budget = tu.smem_budget ? tu.smem_budget : kDefaultBudget[kernel];
+  int R = tu.R ? tu.R : kDefaultR[kernel];
+  const int tensors = kernel ? 2 : 1;
+  const int ncw = static_cast<int>(nc / 32);
+  while (true) {
+    const int64_t stage = static_cast<int64_t>(tensors) * R * row_bytes;
+    int64_t ns = budget / stage;
+    if (ns > 8) ns = 8;
+    if (ns < 2) ns = 2;
+    const size_t extra = 16 * static_cast<size_t>(ns) + (2 * ncw * R * 2 + ncw) * cs + 64;
+    if (static_cast<size_t>(ns * stage) + extra <= static_cast<size_t>(kSmemOptin)) {
+      pl->path = 1;
+      pl->V = V;
+      pl->R = R;
+      pl->NS = static_cast<int>(ns);
+      pl->threads = static_cast<int>(nc) + 32;
+      pl->smem = static_cast<size_t>(ns * stage) + extra;
+      return true;
+    }
+    if (R == 1) return false;
+    R /= 2;
+  }
+}
+
+// kernel: 0 fwd, 1 bwd.  `ptrs` are the row-tensor / modulation pointers that the vector paths
+// read or write with 16-byte accesses.
 int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, int64_t n_tile,
               const void* const* ptrs, int nptrs, Plan* out, bool force_generic = false) {
   int dev, sms;
@@ -192,59 +272,39 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
   const int es = elem_size(dtype);
   const int cs = ct_size(dtype);
   const int epv = 16 / es;
-  bool vec_ok = !tu.force_generic && !force_generic && (D * es) % 16 == 0 && (mod_stride * es) % 16 == 0;
+  bool vec_ok = !tu.force_generic && !force_generic && (D * es) % 16 == 0 &&
+                (mod_stride * es) % 16 == 0;
   for (int i = 0; i < nptrs && vec_ok; ++i) vec_ok = aligned16(ptrs[i]);
   Plan pl;
   if (vec_ok) {
     const int64_t nvec = D / epv;
     const int row_bytes = static_cast<int>(D * es);
-    const int vcap = kernel ? 384 : 256;
-    int V = tu.V;
-    if (V == 0) {
-      V = 4;
-      for (int v : {1, 2, 4})
-        if (((nvec + v - 1) / v + 31) / 32 * 32 <= vcap) {
-          V = v;
-          break;
-        }
+    if (kernel == 0 && tu.V == 0 && tu.R == 0 && nvec <= 32 * kMaxVpl) {
+      // rows-in-registers forward
+      int vi = 0;
+      while (32 * kVpl[vi] < nvec) ++vi;
+      pl.path = 2;
+      pl.V = kVpl[vi];
+      pl.threads = 256;
+      pl.smem = 2 * static_cast<size_t>(D) * cs;
+      // variant 1 = keep packed (re-expand per pass), 2 = compiler's choice; default by width
+      const bool repack = tu.variant ? tu.variant == 1 : kVpl[vi] >= 12;
+      pl.R = repack ? 1 : 0;
+      pl.fn = rows_kernel(dtype, vi, repack);
+    } else if (ring_plan(kernel, nvec, row_bytes, cs, tu, &pl)) {
+      pl.fn = tma_kernel(kernel, dtype, pl.V, pl.R);
     }
-    const int64_t nc = ((nvec + V - 1) / V + 31) / 32 * 32;
-    const int budget = tu.smem_budget ? tu.smem_budget : kDefaultBudget[kernel];
-    int R = tu.R ? tu.R : kDefaultR[kernel];
-    const int tensors = kernel ? 2 : 1;
-    int NS = 0;
-    size_t smem = 0;
-    while (true) {
-      const int64_t stage = static_cast<int64_t>(tensors) * R * row_bytes;
-      int64_t ns = budget / stage;
-      if (ns > 8) ns = 8;
-      if (ns < 2 && stage * 2 <= kSmemOptin - 4096) ns = 2;
-      const int ncw = static_cast<int>(nc / 32);
-      const size_t extra = 16 * static_cast<size_t>(ns) + (2 * ncw * R * 2 + ncw) * cs + 64;
-      if (ns >= 2 && static_cast<size_t>(ns * stage) + extra <= static_cast<size_t>(kSmemOptin)) {
-        NS = static_cast<int>(ns);
-        smem = static_cast<size_t>(ns * stage) + extra;
-        break;
-      }
-      if (R == 1) break;
-      R /= 2;
-    }
-    if (nc + 32 <= kMaxThreads && NS >= 2 && (V == 1 || V == 2 || V == 4) &&
-        (R == 1 || R == 2 || R == 4)) {
-      pl.path = 1;
-      pl.V = V;
-      pl.R = R;
-      pl.NS = NS;
-      pl.threads = static_cast<int>(nc) + 32;
-      pl.smem = smem;
-      pl.fn = tma_kernel(kernel, dtype, V, R);
-      rc = ensure_attr(pl.fn, dev);
-      if (rc) return rc;
+    if (pl.path != 0) {
       int occ = 0;
-      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pl.fn, pl.threads, pl.smem);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-      if (occ < 1) pl.path = 0;
-      else pl.grid = static_cast<int>(std::min<int64_t>(N, static_cast<int64_t>(sms) * occ));
+      rc = occupancy(pl, dev, &occ);
+      if (rc) return rc;
+      if (occ < 1) {
+        pl = Plan();
+      } else {
+        int64_t grid = static_cast<int64_t>(sms) * occ;
+        if (pl.path == 2) grid = std::min<int64_t>(grid, (N + 7) / 8);
+        pl.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, grid)));
+      }
     }
   }
   if (pl.path == 0) {
@@ -286,7 +346,7 @@ int al_abi_version(void) { return 1; }
 const char* al_last_error(void) { return g_err; }
 
 int al_set_tuning(int kernel, int vecs_per_thread, int rows_per_stage, int smem_budget,
-                  int force_generic) {
+                  int force_generic, int variant) {
   if (kernel < 0 || kernel > 1) return fail(AL_ERR_VALUE, "kernel must be 0 or 1");
   if (vecs_per_thread && vecs_per_thread != 1 && vecs_per_thread != 2 && vecs_per_thread != 4)
     return fail(AL_ERR_VALUE, "vecs_per_thread must be 0,1,2,4");
@@ -297,6 +357,7 @@ int al_set_tuning(int kernel, int vecs_per_thread, int rows_per_stage, int smem_
   g_tune[kernel].R = rows_per_stage;
   g_tune[kernel].smem_budget = smem_budget;
   g_tune[kernel].force_generic = force_generic;
+  g_tune[kernel].variant = variant;
   return AL_OK;
 }
 
@@ -311,6 +372,13 @@ int al_device_init(int device) {
       for (int V : {1, 2, 4})
         for (int R : {1, 2, 4}) {
           rc = ensure_attr(tma_kernel(kernel, dt, V, R), device);
+          if (rc) return rc;
+        }
+      if (kernel == 0)
+        for (int vi = 0; vi < kNumVpl; ++vi) {
+          rc = ensure_attr(rows_kernel(dt, vi, false), device);
+          if (rc) return rc;
+          rc = ensure_attr(rows_kernel(dt, vi, true), device);
           if (rc) return rc;
         }
       cudaFuncAttributes fa;

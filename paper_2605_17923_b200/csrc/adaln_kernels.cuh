@@ -109,10 +109,127 @@ struct StageWalker {
 };
 
 // =====================================================================================
-// Forward, TMA ring path.  blockDim = nc consumers (multiple of 32) + 1 producer warp.
+// Forward, row-in-registers path (D up to 32*VPL 16-byte vectors).
+// One warp owns one row at a time: 128-bit streaming loads of the whole row into registers,
+// exact two-pass statistics from registers (warp-shuffle reductions only -- no CTA barrier),
+// then y written with 128-bit streaming stores.  (1+scale, shift) of the CTA's current
+// modulation group are staged once in shared memory as fp32 pairs.  Math runs on packed
+// fp32 pairs (FADD2/FMUL2/FFMA2).  Rows of the CTA's contiguous range are interleaved
+// across its warps; the CTA range is split into modulation-group segments, and only a segment
+// change (a new sample) costs a __syncthreads.
+// =====================================================================================
+template <typename T, int VPL, bool REPACK>
+__global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
+  using CT = typename Traits<T>::CT;
+  using P = typename PairOf<CT>::type;
+  constexpr int EPV = Traits<T>::EPV;
+  constexpr int NP = EPV / 2;  // pairs per 16-byte vector
+  extern __shared__ __align__(16) uint8_t smem[];
+  P* s1 = reinterpret_cast<P*>(smem);  // [nvec * NP] : 1 + scale
+  P* sh = s1 + p.nvec * NP;            // [nvec * NP] : shift
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+  const CT invD = CT(1) / static_cast<CT>(p.D);
+  const CT eps = static_cast<CT>(p.eps);
+  const int RB = p.row_bytes;
+  bool nf = false;
+
+  int64_t row0 = r0;
+  while (row0 < r1) {
+    const int64_t g = row0 / p.S_grp;
+    const int64_t seg_end = min(r1, (g + 1) * p.S_grp);
+    __syncthreads();  // every warp is done with the previous group's modulation
+    {
+      const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
+      const uint8_t* sf = static_cast<const uint8_t*>(p.shift) + g * p.mod_stride * sizeof(T);
+      for (int c = tid; c < p.nvec; c += blockDim.x) {
+        P a[NP], b[NP];
+        unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sc) + c), a);
+        unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sf) + c), b);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y) && finite_ct(b[e].x) && finite_ct(b[e].y));
+          s1[c * NP + e] = add2(a[e], splat2(CT(1)));
+          sh[c * NP + e] = b[e];
+        }
+      }
+    }
+    __syncthreads();
+    for (int64_t row = row0 + warp; row < seg_end; row += nwarp) {
+      const uint8_t* xr = static_cast<const uint8_t*>(p.x) + row * RB;
+      uint4 v[VPL];
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        v[i] = c < p.nvec ? ld_global_nc_v4(xr + c * 16) : make_uint4(0, 0, 0, 0);
+      }
+      // pass 1: mean (zero-filled tail vectors add nothing)
+      P acc[4] = {splat2(CT(0)), splat2(CT(0)), splat2(CT(0)), splat2(CT(0))};
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        P q[NP];
+        if constexpr (REPACK) unpack2_v<T>(v[i], q); else unpack2<T>(v[i], q);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) acc[(i * NP + e) & 3] = add2(acc[(i * NP + e) & 3], q[e]);
+      }
+      P t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+      const CT mean = warp_sum(t.x + t.y) * invD;
+      const P nm = splat2(-mean);
+      // pass 2: sum of squared deviations (valid vectors only)
+      acc[0] = acc[1] = acc[2] = acc[3] = splat2(CT(0));
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        if (lane + 32 * i < p.nvec) {
+          P q[NP];
+          if constexpr (REPACK) unpack2_v<T>(v[i], q); else unpack2<T>(v[i], q);
+#pragma unroll
+          for (int e = 0; e < NP; ++e) {
+            const P d = add2(q[e], nm);
+            acc[(i * NP + e) & 3] = fma2(d, d, acc[(i * NP + e) & 3]);
+          }
+        }
+      }
+      t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+      const CT m2 = warp_sum(t.x + t.y);
+      const CT rs = CT(1) / sqrt(m2 * invD + eps);
+      const P rs2 = splat2(rs);
+      // pass 3: y = (x - mean) * rstd * (1 + scale) + shift
+      uint8_t* yr = static_cast<uint8_t*>(p.y) + row * RB;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        if (c < p.nvec) {
+          P q[NP];
+          if constexpr (REPACK) unpack2_v<T>(v[i], q); else unpack2<T>(v[i], q);
+#pragma unroll
+          for (int e = 0; e < NP; ++e)
+            q[e] = fma2(mul2(add2(q[e], nm), rs2), s1[c * NP + e], sh[c * NP + e]);
+          st_global_cs(yr + c * 16, pack2<T>(q));
+        }
+      }
+      if (lane == 0) {
+        static_cast<CT*>(p.mean)[row] = mean;
+        static_cast<CT*>(p.rstd)[row] = rs;
+        nf |= !(finite_ct(mean) && finite_ct(m2));
+      }
+    }
+    row0 = seg_end;
+  }
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+// =====================================================================================
+// Forward, wide-row TMA ring path (rows too wide for registers).
+// blockDim = nc consumers (multiple of 32) + 1 producer warp.  Stage = R rows streamed into
+// shared memory by 1-D bulk copies; consumer thread t owns 16-byte vectors t + i*nc.
+// Statistics: per-thread two-pass over (x - K) with K = the row's first element (shifted data:
+// exact differences for clustered rows), merged across lanes and warps with the parallel
+// variance identity M2 = sum_i [M2_i + n_i (m_i - m)^2].
 // =====================================================================================
 template <typename T, int V, int R>
-__global__ void __launch_bounds__(512) adaln_fwd_tma(const FwdParams p) {
+__global__ void __launch_bounds__(512) adaln_fwd_wide(const FwdParams p) {
   using CT = typename Traits<T>::CT;
   constexpr int EPV = Traits<T>::EPV;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -218,10 +335,13 @@ __global__ void __launch_bounds__(512) adaln_fwd_tma(const FwdParams p) {
     const uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
     CT* rd = red + (it & 1) * (ncw * R * 2);
 
-    // phase 1: per-row statistics of the owned elements, merged within the warp
+    // phase 1: per-row statistics of the owned elements (shifted by K), merged within the warp
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
       if (rr < rows) {
+        CT kk[EPV];
+        unpack<T>(ld_shared_v4(st + rr * RB), kk);
+        const CT K = kk[0];
         CT v[V][EPV];
         CT sum = CT(0);
 #pragma unroll
@@ -229,7 +349,10 @@ __global__ void __launch_bounds__(512) adaln_fwd_tma(const FwdParams p) {
           if (vmask >> j & 1) {
             unpack<T>(ld_shared_v4(st + rr * RB + (tid + j * nc) * 16), v[j]);
 #pragma unroll
-            for (int e = 0; e < EPV; ++e) sum += v[j][e];
+            for (int e = 0; e < EPV; ++e) {
+              v[j][e] -= K;
+              sum += v[j][e];
+            }
           }
         }
         const CT mt = sum * inv_nt;
@@ -260,12 +383,15 @@ __global__ void __launch_bounds__(512) adaln_fwd_tma(const FwdParams p) {
     for (int rr = 0; rr < R; ++rr) {
       if (rr < rows) {
         const int64_t row = rb + rr;
-        CT mean = CT(0);
-        for (int q = 0; q < ncw; ++q) mean = fma(wcnt[q], rd[(q * R + rr) * 2], mean);
-        mean *= invD;
+        CT kk[EPV];
+        unpack<T>(ld_shared_v4(st + rr * RB), kk);
+        const CT K = kk[0];
+        CT md = CT(0);  // mean of (x - K)
+        for (int q = 0; q < ncw; ++q) md = fma(wcnt[q], rd[(q * R + rr) * 2], md);
+        md *= invD;
         CT m2 = CT(0);
         for (int q = 0; q < ncw; ++q) {
-          const CT d = rd[(q * R + rr) * 2] - mean;
+          const CT d = rd[(q * R + rr) * 2] - md;
           m2 += fma(wcnt[q] * d, d, rd[(q * R + rr) * 2 + 1]);
         }
         const CT rs = CT(1) / sqrt(m2 * invD + eps);
@@ -276,11 +402,12 @@ __global__ void __launch_bounds__(512) adaln_fwd_tma(const FwdParams p) {
             CT v[EPV];
             unpack<T>(ld_shared_v4(st + rr * RB + (tid + j * nc) * 16), v);
 #pragma unroll
-            for (int e = 0; e < EPV; ++e) v[e] = fma((v[e] - mean) * rs, s1[j][e], sh[j][e]);
+            for (int e = 0; e < EPV; ++e) v[e] = fma(((v[e] - K) - md) * rs, s1[j][e], sh[j][e]);
             st_global_cs(yrow + (tid + j * nc) * 16, pack<T>(v));
           }
         }
         if (tid == 0) {
+          const CT mean = K + md;
           static_cast<CT*>(p.mean)[row] = mean;
           static_cast<CT*>(p.rstd)[row] = rs;
           nf |= !(finite_ct(mean) && finite_ct(m2));
@@ -300,11 +427,17 @@ __global__ void __launch_bounds__(512) adaln_fwd_tma(const FwdParams p) {
 
 // =====================================================================================
 // Backward stage 1, TMA ring path.  Stage layout: [x: R rows][dy: R rows].
+// Consumer thread t owns 16-byte column vectors t + i*nc (i < V): per row it forms
+// xhat = (x - mu) * rstd and g = dy * (1 + scale) once, keeps both in registers across the
+// row-sum barrier, folds dy and dy*xhat into its column accumulators, and after the barrier
+// writes dx = rstd * (g - mean(g) - xhat * mean(g*xhat)).  Packed fp32 pair math.
 // =====================================================================================
 template <typename T, int V, int R>
-__global__ void __launch_bounds__(512) adaln_bwd_tma(const BwdParams p) {
+__global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
   using CT = typename Traits<T>::CT;
+  using P = typename PairOf<CT>::type;
   constexpr int EPV = Traits<T>::EPV;
+  constexpr int NP = EPV / 2;
   extern __shared__ __align__(128) uint8_t smem[];
 
   const int nc = blockDim.x - 32;
@@ -369,11 +502,11 @@ __global__ void __launch_bounds__(512) adaln_bwd_tma(const BwdParams p) {
   CT* ws_sh = ws_sc + p.nslots * p.D;
   bool nf = false;
 
-  CT s1[V][EPV], acc_sc[V][EPV], acc_sh[V][EPV];
+  P s1[V][NP], acc_sc[V][NP], acc_sh[V][NP];
 #pragma unroll
   for (int j = 0; j < V; ++j)
 #pragma unroll
-    for (int e = 0; e < EPV; ++e) acc_sc[j][e] = acc_sh[j][e] = CT(0);
+    for (int e = 0; e < NP; ++e) acc_sc[j][e] = acc_sh[j][e] = splat2(CT(0));
   int64_t cur_g = -1;
 
   auto flush = [&](int64_t g) {
@@ -382,22 +515,14 @@ __global__ void __launch_bounds__(512) adaln_bwd_tma(const BwdParams p) {
     for (int j = 0; j < V; ++j) {
       if (vmask >> j & 1) {
         const int64_t col = static_cast<int64_t>(tid + j * nc) * EPV;
-        CT* a = ws_sc + slot * p.D + col;
-        CT* b = ws_sh + slot * p.D + col;
+        P* a = reinterpret_cast<P*>(ws_sc + slot * p.D + col);
+        P* b = reinterpret_cast<P*>(ws_sh + slot * p.D + col);
 #pragma unroll
-        for (int e = 0; e < EPV; e += 16 / sizeof(CT)) {
-          if constexpr (sizeof(CT) == 4) {
-            *reinterpret_cast<float4*>(a + e) =
-                make_float4(acc_sc[j][e], acc_sc[j][e + 1], acc_sc[j][e + 2], acc_sc[j][e + 3]);
-            *reinterpret_cast<float4*>(b + e) =
-                make_float4(acc_sh[j][e], acc_sh[j][e + 1], acc_sh[j][e + 2], acc_sh[j][e + 3]);
-          } else {
-            *reinterpret_cast<double2*>(a + e) = make_double2(acc_sc[j][e], acc_sc[j][e + 1]);
-            *reinterpret_cast<double2*>(b + e) = make_double2(acc_sh[j][e], acc_sh[j][e + 1]);
-          }
+        for (int e = 0; e < NP; ++e) {
+          a[e] = acc_sc[j][e];
+          b[e] = acc_sh[j][e];
+          acc_sc[j][e] = acc_sh[j][e] = splat2(CT(0));
         }
-#pragma unroll
-        for (int e = 0; e < EPV; ++e) acc_sc[j][e] = acc_sh[j][e] = CT(0);
       }
     }
   };
@@ -412,7 +537,7 @@ __global__ void __launch_bounds__(512) adaln_bwd_tma(const BwdParams p) {
   StageWalker wp = w;
   CT mcur[R], rcur[R];
   {
-    int64_t st0, g0;
+    int64_t st0 = 0, g0;
     const int n0 = wp.done() ? 0 : wp.next(R, st0, g0);
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
@@ -441,10 +566,10 @@ __global__ void __launch_bounds__(512) adaln_bwd_tma(const BwdParams p) {
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         if (vmask >> j & 1) {
-          unpack<T>(__ldg(reinterpret_cast<const uint4*>(sc + static_cast<size_t>(tid + j * nc) * 16)),
-                    s1[j]);
+          unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sc + static_cast<size_t>(tid + j * nc) * 16)),
+                     s1[j]);
 #pragma unroll
-          for (int e = 0; e < EPV; ++e) s1[j][e] += CT(1);
+          for (int e = 0; e < NP; ++e) s1[j][e] = add2(s1[j][e], splat2(CT(1)));
         }
       }
     }
@@ -454,71 +579,67 @@ __global__ void __launch_bounds__(512) adaln_bwd_tma(const BwdParams p) {
     CT* rd = red + (it & 1) * (ncw * R * 2);
 
     // phase 1: row sums of g and g*xhat; column accumulators of dy and dy*xhat
+    P xh[R][V][NP], gg[R][V][NP];
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
       if (rr < rows) {
-        const CT m = mcur[rr], r = rcur[rr];
-        CT sg = CT(0), sgx = CT(0);
+        const P nm = splat2(-mcur[rr]), r2 = splat2(rcur[rr]);
+        P sg = splat2(CT(0)), sgx = splat2(CT(0));
 #pragma unroll
         for (int j = 0; j < V; ++j) {
           if (vmask >> j & 1) {
-            CT xv[EPV], dv[EPV];
-            unpack<T>(ld_shared_v4(stx + rr * RB + (tid + j * nc) * 16), xv);
-            unpack<T>(ld_shared_v4(std_ + rr * RB + (tid + j * nc) * 16), dv);
+            P xv[NP], dv[NP];
+            unpack2<T>(ld_shared_v4(stx + rr * RB + (tid + j * nc) * 16), xv);
+            unpack2<T>(ld_shared_v4(std_ + rr * RB + (tid + j * nc) * 16), dv);
 #pragma unroll
-            for (int e = 0; e < EPV; ++e) {
-              const CT xh = (xv[e] - m) * r;
-              const CT gg = dv[e] * s1[j][e];
-              sg += gg;
-              sgx = fma(gg, xh, sgx);
-              acc_sh[j][e] += dv[e];
-              acc_sc[j][e] = fma(dv[e], xh, acc_sc[j][e]);
+            for (int e = 0; e < NP; ++e) {
+              xh[rr][j][e] = mul2(add2(xv[e], nm), r2);
+              gg[rr][j][e] = mul2(dv[e], s1[j][e]);
+              sg = add2(sg, gg[rr][j][e]);
+              sgx = fma2(gg[rr][j][e], xh[rr][j][e], sgx);
+              acc_sh[j][e] = add2(acc_sh[j][e], dv[e]);
+              acc_sc[j][e] = fma2(dv[e], xh[rr][j][e], acc_sc[j][e]);
             }
           }
         }
-        sg = warp_sum(sg);
-        sgx = warp_sum(sgx);
+        const CT tsg = warp_sum(sg.x + sg.y);
+        const CT tsgx = warp_sum(sgx.x + sgx.y);
         if (lane == 0) {
-          rd[(warp * R + rr) * 2 + 0] = sg;
-          rd[(warp * R + rr) * 2 + 1] = sgx;
+          rd[(warp * R + rr) * 2 + 0] = tsg;
+          rd[(warp * R + rr) * 2 + 1] = tsgx;
         }
       }
     }
     named_bar_sync(1, nc);
+    // every consumer has read this stage into registers: release the slot to the producer
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
 
     // phase 2: dx = rstd * (g - mean(g) - xhat * mean(g*xhat))
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
       if (rr < rows) {
         const int64_t row = rb + rr;
-        const CT m = mcur[rr], r = rcur[rr];
         CT tg = CT(0), tgx = CT(0);
         for (int q = 0; q < ncw; ++q) {
           tg += rd[(q * R + rr) * 2 + 0];
           tgx += rd[(q * R + rr) * 2 + 1];
         }
-        const CT mg = tg * invD, mgx = tgx * invD;
+        const P nmg = splat2(-tg * invD), nmgx = splat2(-tgx * invD), r2 = splat2(rcur[rr]);
         uint8_t* dxrow = static_cast<uint8_t*>(p.dx) + row * RB;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
           if (vmask >> j & 1) {
-            CT xv[EPV], dv[EPV];
-            unpack<T>(ld_shared_v4(stx + rr * RB + (tid + j * nc) * 16), xv);
-            unpack<T>(ld_shared_v4(std_ + rr * RB + (tid + j * nc) * 16), dv);
+            P o[NP];
 #pragma unroll
-            for (int e = 0; e < EPV; ++e) {
-              const CT xh = (xv[e] - m) * r;
-              const CT gg = dv[e] * s1[j][e];
-              xv[e] = r * fma(-xh, mgx, gg - mg);
-            }
-            st_global_cs(dxrow + (tid + j * nc) * 16, pack<T>(xv));
+            for (int e = 0; e < NP; ++e)
+              o[e] = mul2(fma2(xh[rr][j][e], nmgx, add2(gg[rr][j][e], nmg)), r2);
+            st_global_cs(dxrow + (tid + j * nc) * 16, pack2<T>(o));
           }
         }
         if (tid == 0) nf |= !(finite_ct(tg) && finite_ct(tgx));
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
     if (++s == NS) {
       s = 0;
       ph ^= 1;

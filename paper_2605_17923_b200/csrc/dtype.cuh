@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <type_traits>
 
 namespace al {
 
@@ -121,6 +122,131 @@ __device__ __forceinline__ uint4 pack<__half>(const float* i) {
     w[k] = *reinterpret_cast<uint32_t*>(&h);
   }
   return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// ---- packed pairs: fp32 math runs two lanes per instruction (sm_100 FADD2/FMUL2/FFMA2) -------
+template <typename CT>
+struct PairOf;
+template <>
+struct PairOf<float> {
+  using type = float2;
+};
+template <>
+struct PairOf<double> {
+  using type = double2;
+};
+
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ double2 add2(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 mul2(double2 a, double2 b) {
+  return make_double2(a.x * b.x, a.y * b.y);
+}
+__device__ __forceinline__ double2 fma2(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
+}
+__device__ __forceinline__ float2 splat2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ double2 splat2(double v) { return make_double2(v, v); }
+
+// 16-byte vector <-> EPV/2 pairs in the compute type
+template <typename T>
+__device__ __forceinline__ void unpack2(const uint4& v, typename PairOf<typename Traits<T>::CT>::type* o);
+template <>
+__device__ __forceinline__ void unpack2<float>(const uint4& v, float2* o) {
+  o[0] = make_float2(__uint_as_float(v.x), __uint_as_float(v.y));
+  o[1] = make_float2(__uint_as_float(v.z), __uint_as_float(v.w));
+}
+template <>
+__device__ __forceinline__ void unpack2<double>(const uint4& v, double2* o) {
+  o[0] = make_double2(__hiloint2double(static_cast<int>(v.y), static_cast<int>(v.x)),
+                      __hiloint2double(static_cast<int>(v.w), static_cast<int>(v.z)));
+}
+template <>
+__device__ __forceinline__ void unpack2<__nv_bfloat16>(const uint4& v, float2* o) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    o[i] = make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xffff0000u));
+}
+template <>
+__device__ __forceinline__ void unpack2<__half>(const uint4& v, float2* o) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) o[i] = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+}
+
+// Same as unpack2, but through volatile asm so the compiler re-expands the packed registers at
+// every use instead of keeping the whole row unpacked (register pressure vs. ALU trade-off).
+template <typename T>
+__device__ __forceinline__ void unpack2_v(const uint4& v, typename PairOf<typename Traits<T>::CT>::type* o) {
+  if constexpr (sizeof(T) == 2) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t lo, hi;
+      if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        asm volatile("shl.b32 %0, %2, 16;\n\tand.b32 %1, %2, 0xffff0000;"
+                     : "=r"(lo), "=r"(hi) : "r"(w[i]));
+        o[i] = make_float2(__uint_as_float(lo), __uint_as_float(hi));
+      } else {
+        uint32_t ww;
+        asm volatile("mov.b32 %0, %1;" : "=r"(ww) : "r"(w[i]));
+        o[i] = __half22float2(*reinterpret_cast<const __half2*>(&ww));
+      }
+    }
+  } else {
+    uint4 c;
+    asm volatile("mov.b32 %0, %4;\n\tmov.b32 %1, %5;\n\tmov.b32 %2, %6;\n\tmov.b32 %3, %7;"
+                 : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w)
+                 : "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+    unpack2<T>(c, o);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ uint4 pack2(const typename PairOf<typename Traits<T>::CT>::type* in);
+template <>
+__device__ __forceinline__ uint4 pack2<float>(const float2* i) {
+  return make_uint4(__float_as_uint(i[0].x), __float_as_uint(i[0].y), __float_as_uint(i[1].x),
+                    __float_as_uint(i[1].y));
+}
+template <>
+__device__ __forceinline__ uint4 pack2<double>(const double2* i) {
+  return make_uint4(static_cast<uint32_t>(__double2loint(i[0].x)),
+                    static_cast<uint32_t>(__double2hiint(i[0].x)),
+                    static_cast<uint32_t>(__double2loint(i[0].y)),
+                    static_cast<uint32_t>(__double2hiint(i[0].y)));
+}
+template <>
+__device__ __forceinline__ uint4 pack2<__nv_bfloat16>(const float2* i) {
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    __nv_bfloat162 h = __float22bfloat162_rn(i[k]);
+    w[k] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+template <>
+__device__ __forceinline__ uint4 pack2<__half>(const float2* i) {
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    __half2 h = __float22half2_rn(i[k]);
+    w[k] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ uint4 ld_global_nc_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
 }
 
 template <typename CT>

@@ -32,16 +32,16 @@ def test_library_exports_every_header_symbol():
 def test_library_is_sm100a():
     log = (_build.LIBDIR / "ptxas.log").read_text()
     assert "for 'sm_100a'" in log
-    assert "adaln_fwd_tma" in log and "adaln_bwd_tma" in log and "adaln_bwd_reduce" in log
+    assert "adaln_fwd_rows" in log and "adaln_fwd_wide" in log and "adaln_bwd_tma" in log and "adaln_bwd_reduce" in log
 
 
 def test_abi_version_and_errors_without_gpu():
     lib = nat.load()
     assert lib.al_abi_version() == nat.ABI_VERSION
     # argument validation happens before any CUDA call
-    assert lib.al_set_tuning(2, 0, 0, 0, 0) == nat.AL_ERR_VALUE
+    assert lib.al_set_tuning(2, 0, 0, 0, 0, 0) == nat.AL_ERR_VALUE
     assert "kernel" in nat.last_error()
-    assert lib.al_set_tuning(0, 3, 0, 0, 0) == nat.AL_ERR_VALUE
+    assert lib.al_set_tuning(0, 3, 0, 0, 0, 0) == nat.AL_ERR_VALUE
     assert lib.al_adaln_forward(None, None, None, None, None, None, 1, 4, 0, 0, nat.AL_F32,
                                 1e-6, None, None) == nat.AL_ERR_SHAPE
     assert lib.al_adaln_forward(None, None, None, None, None, None, 1, 4, 8, 0, 9, 1e-6, None,
