@@ -288,7 +288,7 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
       pl.threads = 256;
       pl.smem = 2 * static_cast<size_t>(D) * cs;
       // variant 1 = keep packed (re-expand per pass), 2 = compiler's choice; default by width
-      const bool repack = tu.variant ? tu.variant == 1 : kVpl[vi] >= 12;
+      const bool repack = tu.variant == 1;
       pl.R = repack ? 1 : 0;
       pl.fn = rows_kernel(dtype, vi, repack);
     } else if (ring_plan(kernel, nvec, row_bytes, cs, tu, &pl)) {

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
   using P = typename PairOf<CT>::type;
   constexpr int EPV = Traits<T>::EPV;
   constexpr int NP = EPV / 2;  // pairs per 16-byte vector
+  constexpr bool SHIFT = sizeof(T) >= 4;
   extern __shared__ __align__(16) uint8_t smem[];
   P* s1 = reinterpret_cast<P*>(smem);  // [nvec * NP] : 1 + scale
   P* sh = s1 + p.nvec * NP;            // [nvec * NP] : shift
@@ -165,18 +166,34 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
         const int c = lane + 32 * i;
         v[i] = c < p.nvec ? ld_global_nc_v4(xr + c * 16) : make_uint4(0, 0, 0, 0);
       }
+      // 32-bit/64-bit inputs: statistics of (x - K), K = the row's first element, so that rows
+      // with a large common offset keep full precision in the fp32 sums (x - K is exact for
+      // clustered values).  16-bit inputs skip the shift: their own rounding dominates.
+      CT K = CT(0);
+      if constexpr (SHIFT) {
+        P q0[NP];
+        unpack2<T>(v[0], q0);
+        K = __shfl_sync(0xffffffffu, q0[0].x, 0);
+      }
+      const P nK = splat2(-K);
       // pass 1: mean (zero-filled tail vectors add nothing)
       P acc[4] = {splat2(CT(0)), splat2(CT(0)), splat2(CT(0)), splat2(CT(0))};
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
-        P q[NP];
-        if constexpr (REPACK) unpack2_v<T>(v[i], q); else unpack2<T>(v[i], q);
+        if (!SHIFT || lane + 32 * i < p.nvec) {
+          P q[NP];
+          if constexpr (REPACK) unpack2_v<T>(v[i], q); else unpack2<T>(v[i], q);
 #pragma unroll
-        for (int e = 0; e < NP; ++e) acc[(i * NP + e) & 3] = add2(acc[(i * NP + e) & 3], q[e]);
+          for (int e = 0; e < NP; ++e) {
+            if constexpr (SHIFT) q[e] = add2(q[e], nK);
+            acc[(i * NP + e) & 3] = add2(acc[(i * NP + e) & 3], q[e]);
+          }
+        }
       }
       P t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
-      const CT mean = warp_sum(t.x + t.y) * invD;
-      const P nm = splat2(-mean);
+      const CT md = warp_sum(t.x + t.y) * invD;  // mean of (x - K)
+      const CT mean = K + md;
+      const P nm = splat2(SHIFT ? -md : -mean);
       // pass 2: sum of squared deviations (valid vectors only)
       acc[0] = acc[1] = acc[2] = acc[3] = splat2(CT(0));
 #pragma unroll
@@ -186,6 +203,7 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
           if constexpr (REPACK) unpack2_v<T>(v[i], q); else unpack2<T>(v[i], q);
 #pragma unroll
           for (int e = 0; e < NP; ++e) {
+            if constexpr (SHIFT) q[e] = add2(q[e], nK);
             const P d = add2(q[e], nm);
             acc[(i * NP + e) & 3] = fma2(d, d, acc[(i * NP + e) & 3]);
           }
@@ -204,8 +222,10 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
           P q[NP];
           if constexpr (REPACK) unpack2_v<T>(v[i], q); else unpack2<T>(v[i], q);
 #pragma unroll
-          for (int e = 0; e < NP; ++e)
+          for (int e = 0; e < NP; ++e) {
+            if constexpr (SHIFT) q[e] = add2(q[e], nK);
             q[e] = fma2(mul2(add2(q[e], nm), rs2), s1[c * NP + e], sh[c * NP + e]);
+          }
           st_global_cs(yr + c * 16, pack2<T>(q));
         }
       }
