@@ -76,7 +76,7 @@ constexpr int kMaxVpl = 24;
 template <typename T>
 struct Table {
   FwdFn rows[kNumVpl];
-  FwdFn rows_rp[kNumVpl];  // REPACK variant
+  FwdFn rows_rp[kNumVpl];  // PACKED variant (row kept packed, re-expanded per pass)
   FwdFn wide[3][3];  // [V idx][R idx], V in {1,2,4}, R in {1,2,4}
   BwdFn bwd[3][3];
   FwdFn fwd_generic;
@@ -524,7 +524,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   int64_t G64 = pl.grid;
   void* rargs[] = {&workspace, &dscale, &dshift, &p.N, &p.S_grp, &p.D, &G64, &p.nslots};
   dim3 rgrid(static_cast<unsigned>((dim + 31) / 32), static_cast<unsigned>(ngroups));
-  e = cudaLaunchKernel(rk, rgrid, dim3(256), rargs, 0, st);
+  e = cudaLaunchKernel(rk, rgrid, dim3(1024), rargs, 0, st);
   if (e != cudaSuccess) return cuda_fail(e, "backward stage-2 launch");
   return AL_OK;
 }

@@ -117,8 +117,11 @@ struct StageWalker {
 // fp32 pairs (FADD2/FMUL2/FFMA2).  Rows of the CTA's contiguous range are interleaved
 // across its warps; the CTA range is split into modulation-group segments, and only a segment
 // change (a new sample) costs a __syncthreads.
+// PACKED = true keeps the row packed in registers and re-expands it in every pass (more ALU,
+// about half the registers -> twice the resident warps); false lets the compiler keep it
+// expanded.
 // =====================================================================================
-template <typename T, int VPL, bool REPACK>
+template <typename T, int VPL, bool PACKED>
 __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
@@ -136,6 +139,12 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
   const CT eps = static_cast<CT>(p.eps);
   const int RB = p.row_bytes;
   bool nf = false;
+
+  // expand vector i of the row; with PACKED the expansion depends on the runtime zero z
+  auto expand = [&](const uint4& raw, uint32_t z, P* q) {
+    if constexpr (PACKED) unpack2_dep<T>(raw, z, q);
+    else unpack2<T>(raw, q);
+  };
 
   int64_t row0 = r0;
   while (row0 < r1) {
@@ -182,7 +191,7 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
       for (int i = 0; i < VPL; ++i) {
         if (!SHIFT || lane + 32 * i < p.nvec) {
           P q[NP];
-          if constexpr (REPACK) unpack2_v<T>(v[i], q); else unpack2<T>(v[i], q);
+          expand(v[i], 0u, q);
 #pragma unroll
           for (int e = 0; e < NP; ++e) {
             if constexpr (SHIFT) q[e] = add2(q[e], nK);
@@ -194,13 +203,14 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
       const CT md = warp_sum(t.x + t.y) * invD;  // mean of (x - K)
       const CT mean = K + md;
       const P nm = splat2(SHIFT ? -md : -mean);
+      const uint32_t z1 = PACKED ? runtime_zero(md) : 0u;
       // pass 2: sum of squared deviations (valid vectors only)
       acc[0] = acc[1] = acc[2] = acc[3] = splat2(CT(0));
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
         if (lane + 32 * i < p.nvec) {
           P q[NP];
-          if constexpr (REPACK) unpack2_v<T>(v[i], q); else unpack2<T>(v[i], q);
+          expand(v[i], z1, q);
 #pragma unroll
           for (int e = 0; e < NP; ++e) {
             if constexpr (SHIFT) q[e] = add2(q[e], nK);
@@ -213,18 +223,42 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
       const CT m2 = warp_sum(t.x + t.y);
       const CT rs = CT(1) / sqrt(m2 * invD + eps);
       const P rs2 = splat2(rs);
+      const uint32_t z2 = PACKED ? runtime_zero(rs) : 0u;
       // pass 3: y = (x - mean) * rstd * (1 + scale) + shift
       uint8_t* yr = static_cast<uint8_t*>(p.y) + row * RB;
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
         const int c = lane + 32 * i;
         if (c < p.nvec) {
-          P q[NP];
-          if constexpr (REPACK) unpack2_v<T>(v[i], q); else unpack2<T>(v[i], q);
+          P q[NP], a[NP], b[NP];
+          expand(v[i], z2, q);
+          if constexpr (PACKED) {
+            // modulation pairs read after the statistic is known (no early hoisting)
+#pragma unroll
+            for (int e = 0; e < NP; e += 2) {
+              const uint4 ua = ld_shared_v4_dep(&s1[c * NP + e], z2);
+              const uint4 ub = ld_shared_v4_dep(&sh[c * NP + e], z2);
+              if constexpr (sizeof(CT) == 4) {
+                a[e] = make_float2(__uint_as_float(ua.x), __uint_as_float(ua.y));
+                a[e + 1] = make_float2(__uint_as_float(ua.z), __uint_as_float(ua.w));
+                b[e] = make_float2(__uint_as_float(ub.x), __uint_as_float(ub.y));
+                b[e + 1] = make_float2(__uint_as_float(ub.z), __uint_as_float(ub.w));
+              } else {
+                unpack2<double>(ua, &a[e]);
+                unpack2<double>(ub, &b[e]);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < NP; ++e) {
+              a[e] = s1[c * NP + e];
+              b[e] = sh[c * NP + e];
+            }
+          }
 #pragma unroll
           for (int e = 0; e < NP; ++e) {
             if constexpr (SHIFT) q[e] = add2(q[e], nK);
-            q[e] = fma2(mul2(add2(q[e], nm), rs2), s1[c * NP + e], sh[c * NP + e]);
+            q[e] = fma2(mul2(add2(q[e], nm), rs2), a[e], b[e]);
           }
           st_global_cs(yr + c * 16, pack2<T>(q));
         }
@@ -512,9 +546,12 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
 
   // ---------------- consumers ----------------
   uint32_t vmask = 0;
+  int coff[V];  // byte offset of owned vector j inside a row
 #pragma unroll
-  for (int j = 0; j < V; ++j)
+  for (int j = 0; j < V; ++j) {
+    coff[j] = (tid + j * nc) * 16;
     if (tid + j * nc < p.nvec) vmask |= 1u << j;
+  }
   const CT invD = CT(1) / static_cast<CT>(p.D);
   const CT* mean_p = static_cast<const CT*>(p.mean);
   const CT* rstd_p = static_cast<const CT*>(p.rstd);
@@ -534,7 +571,7 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       if (vmask >> j & 1) {
-        const int64_t col = static_cast<int64_t>(tid + j * nc) * EPV;
+        const int64_t col = static_cast<int64_t>(coff[j] / 16) * EPV;
         P* a = reinterpret_cast<P*>(ws_sc + slot * p.D + col);
         P* b = reinterpret_cast<P*>(ws_sh + slot * p.D + col);
 #pragma unroll
@@ -586,10 +623,12 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         if (vmask >> j & 1) {
-          unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sc + static_cast<size_t>(tid + j * nc) * 16)),
-                     s1[j]);
+          unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sc + coff[j])), s1[j]);
 #pragma unroll
           for (int e = 0; e < NP; ++e) s1[j][e] = add2(s1[j][e], splat2(CT(1)));
+        } else {
+#pragma unroll
+          for (int e = 0; e < NP; ++e) s1[j][e] = splat2(CT(0));
         }
       }
     }
@@ -598,54 +637,63 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
     const uint8_t* std_ = stx + R * RB;
     CT* rd = red + (it & 1) * (ncw * R * 2);
 
-    // phase 1: row sums of g and g*xhat; column accumulators of dy and dy*xhat
+    // phase 1: row sums of g and g*xhat; column accumulators of dy and dy*xhat.
+    // Rows past `rows` (stage tail) and columns past D read as zero, so every lane runs the
+    // same instruction stream and the shuffles below are convergent.
     P xh[R][V][NP], gg[R][V][NP];
+    CT rowsum[R * 2];
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      if (rr < rows) {
-        const P nm = splat2(-mcur[rr]), r2 = splat2(rcur[rr]);
-        P sg = splat2(CT(0)), sgx = splat2(CT(0));
+      const bool live = rr < rows;
+      const P nm = splat2(-mcur[rr]), r2 = splat2(rcur[rr]);
+      P sg = splat2(CT(0)), sgx = splat2(CT(0));
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-          if (vmask >> j & 1) {
-            P xv[NP], dv[NP];
-            unpack2<T>(ld_shared_v4(stx + rr * RB + (tid + j * nc) * 16), xv);
-            unpack2<T>(ld_shared_v4(std_ + rr * RB + (tid + j * nc) * 16), dv);
+      for (int j = 0; j < V; ++j) {
+        const bool ok = live && (vmask >> j & 1);
+        P xv[NP], dv[NP];
+        unpack2<T>(ok ? ld_shared_v4(stx + rr * RB + coff[j]) : make_uint4(0, 0, 0, 0), xv);
+        unpack2<T>(ok ? ld_shared_v4(std_ + rr * RB + coff[j]) : make_uint4(0, 0, 0, 0), dv);
 #pragma unroll
-            for (int e = 0; e < NP; ++e) {
-              xh[rr][j][e] = mul2(add2(xv[e], nm), r2);
-              gg[rr][j][e] = mul2(dv[e], s1[j][e]);
-              sg = add2(sg, gg[rr][j][e]);
-              sgx = fma2(gg[rr][j][e], xh[rr][j][e], sgx);
-              acc_sh[j][e] = add2(acc_sh[j][e], dv[e]);
-              acc_sc[j][e] = fma2(dv[e], xh[rr][j][e], acc_sc[j][e]);
-            }
-          }
-        }
-        const CT tsg = warp_sum(sg.x + sg.y);
-        const CT tsgx = warp_sum(sgx.x + sgx.y);
-        if (lane == 0) {
-          rd[(warp * R + rr) * 2 + 0] = tsg;
-          rd[(warp * R + rr) * 2 + 1] = tsgx;
+        for (int e = 0; e < NP; ++e) {
+          xh[rr][j][e] = mul2(add2(xv[e], nm), r2);
+          gg[rr][j][e] = mul2(dv[e], s1[j][e]);
+          sg = add2(sg, gg[rr][j][e]);
+          sgx = fma2(gg[rr][j][e], xh[rr][j][e], sgx);
+          acc_sh[j][e] = add2(acc_sh[j][e], dv[e]);
+          acc_sc[j][e] = fma2(dv[e], xh[rr][j][e], acc_sc[j][e]);
         }
       }
+      rowsum[2 * rr] = sg.x + sg.y;
+      rowsum[2 * rr + 1] = sgx.x + sgx.y;
+    }
+#pragma unroll
+    for (int q = 0; q < 2 * R; ++q) rowsum[q] = warp_sum(rowsum[q]);
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < 2 * R; ++q) rd[warp * 2 * R + q] = rowsum[q];
     }
     named_bar_sync(1, nc);
     // every consumer has read this stage into registers: release the slot to the producer
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
+    // cross-warp totals (fixed warp order -> deterministic)
+    CT tot[2 * R];
+#pragma unroll
+    for (int q = 0; q < 2 * R; ++q) tot[q] = CT(0);
+    for (int q = 0; q < ncw; ++q) {
+      const CT* src = rd + q * 2 * R;
+#pragma unroll
+      for (int u = 0; u < 2 * R; ++u) tot[u] += src[u];
+    }
+
     // phase 2: dx = rstd * (g - mean(g) - xhat * mean(g*xhat))
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
       if (rr < rows) {
         const int64_t row = rb + rr;
-        CT tg = CT(0), tgx = CT(0);
-        for (int q = 0; q < ncw; ++q) {
-          tg += rd[(q * R + rr) * 2 + 0];
-          tgx += rd[(q * R + rr) * 2 + 1];
-        }
-        const P nmg = splat2(-tg * invD), nmgx = splat2(-tgx * invD), r2 = splat2(rcur[rr]);
+        const P nmg = splat2(-tot[2 * rr] * invD), nmgx = splat2(-tot[2 * rr + 1] * invD);
+        const P r2 = splat2(rcur[rr]);
         uint8_t* dxrow = static_cast<uint8_t*>(p.dx) + row * RB;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
@@ -654,10 +702,10 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
 #pragma unroll
             for (int e = 0; e < NP; ++e)
               o[e] = mul2(fma2(xh[rr][j][e], nmgx, add2(gg[rr][j][e], nmg)), r2);
-            st_global_cs(dxrow + (tid + j * nc) * 16, pack2<T>(o));
+            st_global_cs(dxrow + coff[j], pack2<T>(o));
           }
         }
-        if (tid == 0) nf |= !(finite_ct(tg) && finite_ct(tgx));
+        if (tid == 0) nf |= !(finite_ct(tot[2 * rr]) && finite_ct(tot[2 * rr + 1]));
       }
     }
     if (++s == NS) {
@@ -677,15 +725,16 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
 
 // =====================================================================================
 // Backward stage 2: dscale/dshift[g, d] = sum over the CTAs covering group g, ascending.
-// grid = (ceil(D/32), ngroups), block = 256 (8 slot lanes x 32 columns).
+// grid = (ceil(D/32), ngroups), block = 1024: 32 columns x 32 slot lanes; each thread keeps
+// several independent loads in flight, then the 32 slot lanes are combined in a fixed order.
 // =====================================================================================
 template <typename CT>
-__global__ void __launch_bounds__(256) adaln_bwd_reduce(const CT* __restrict__ ws,
-                                                        CT* __restrict__ dscale,
-                                                        CT* __restrict__ dshift, int64_t N,
-                                                        int64_t S_grp, int64_t D, int64_t G,
-                                                        int64_t nslots) {
-  __shared__ double part[2][8][33];
+__global__ void __launch_bounds__(1024) adaln_bwd_reduce(const CT* __restrict__ ws,
+                                                         CT* __restrict__ dscale,
+                                                         CT* __restrict__ dshift, int64_t N,
+                                                         int64_t S_grp, int64_t D, int64_t G,
+                                                         int64_t nslots) {
+  __shared__ double part[2][32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t g = blockIdx.y;
   const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + lane;
@@ -694,26 +743,35 @@ __global__ void __launch_bounds__(256) adaln_bwd_reduce(const CT* __restrict__ w
   const int64_t kf = part_owner(first_row, N, G), kl = part_owner(last_row, N, G);
   double a = 0.0, b = 0.0;
   if (col < D) {
-    const CT* sc = ws + col;
-    const CT* sh = ws + nslots * D + col;
-#pragma unroll 4
-    for (int64_t kk = kf + w; kk <= kl; kk += 8) {
-      a += static_cast<double>(sc[(kk + g) * D]);
-      b += static_cast<double>(sh[(kk + g) * D]);
+    const CT* sc = ws + (kf + g) * D + col;
+    const CT* sh = ws + (nslots + kf + g) * D + col;
+    const int64_t n = kl - kf + 1;
+    int64_t i = w;
+    for (; i + 96 < n; i += 128) {
+      const CT a0 = sc[i * D], a1 = sc[(i + 32) * D], a2 = sc[(i + 64) * D], a3 = sc[(i + 96) * D];
+      const CT b0 = sh[i * D], b1 = sh[(i + 32) * D], b2 = sh[(i + 64) * D], b3 = sh[(i + 96) * D];
+      a += static_cast<double>(a0);
+      a += static_cast<double>(a1);
+      a += static_cast<double>(a2);
+      a += static_cast<double>(a3);
+      b += static_cast<double>(b0);
+      b += static_cast<double>(b1);
+      b += static_cast<double>(b2);
+      b += static_cast<double>(b3);
+    }
+    for (; i < n; i += 32) {
+      a += static_cast<double>(sc[i * D]);
+      b += static_cast<double>(sh[i * D]);
     }
   }
   part[0][w][lane] = a;
   part[1][w][lane] = b;
   __syncthreads();
-  if (w == 0 && col < D) {
-    double ta = 0.0, tb = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      ta += part[0][q][lane];
-      tb += part[1][q][lane];
-    }
-    dscale[g * D + col] = static_cast<CT>(ta);
-    dshift[g * D + col] = static_cast<CT>(tb);
+  if (w < 2 && col < D) {
+    double t = 0.0;
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) t += part[w][q][lane];
+    (w == 0 ? dscale : dshift)[g * D + col] = static_cast<CT>(t);
   }
 }
 

@@ -178,32 +178,44 @@ __device__ __forceinline__ void unpack2<__half>(const uint4& v, float2* o) {
   for (int i = 0; i < 4; ++i) o[i] = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
 }
 
-// Same as unpack2, but through volatile asm so the compiler re-expands the packed registers at
-// every use instead of keeping the whole row unpacked (register pressure vs. ALU trade-off).
+// Same as unpack2, but each expansion carries a true data dependency on `z`, a runtime zero
+// derived from a per-row statistic: ptxas cannot hoist the expansion ahead of that statistic,
+// so a register-resident row stays packed between passes instead of living unpacked
+// (bf16: PRMT against z; other types: OR with z).
+__device__ __forceinline__ uint32_t runtime_zero(float stat) {
+  uint32_t z;
+  asm("{\n\t.reg .pred p;\n\tsetp.nan.f32 p, %1, %1;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(z) : "f"(stat));
+  return z;
+}
+__device__ __forceinline__ uint32_t runtime_zero(double stat) {
+  uint32_t z;
+  asm("{\n\t.reg .pred p;\n\tsetp.nan.f64 p, %1, %1;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(z) : "d"(stat));
+  return z;
+}
+
 template <typename T>
-__device__ __forceinline__ void unpack2_v(const uint4& v, typename PairOf<typename Traits<T>::CT>::type* o) {
-  if constexpr (sizeof(T) == 2) {
+__device__ __forceinline__ void unpack2_dep(const uint4& v, uint32_t z,
+                                            typename PairOf<typename Traits<T>::CT>::type* o) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       uint32_t lo, hi;
-      if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-        asm volatile("shl.b32 %0, %2, 16;\n\tand.b32 %1, %2, 0xffff0000;"
-                     : "=r"(lo), "=r"(hi) : "r"(w[i]));
-        o[i] = make_float2(__uint_as_float(lo), __uint_as_float(hi));
-      } else {
-        uint32_t ww;
-        asm volatile("mov.b32 %0, %1;" : "=r"(ww) : "r"(w[i]));
-        o[i] = __half22float2(*reinterpret_cast<const __half2*>(&ww));
-      }
+      asm("prmt.b32 %0, %1, %2, 0x1044;" : "=r"(lo) : "r"(w[i]), "r"(z));
+      asm("prmt.b32 %0, %1, %2, 0x3244;" : "=r"(hi) : "r"(w[i]), "r"(z));
+      o[i] = make_float2(__uint_as_float(lo), __uint_as_float(hi));
     }
   } else {
-    uint4 c;
-    asm volatile("mov.b32 %0, %4;\n\tmov.b32 %1, %5;\n\tmov.b32 %2, %6;\n\tmov.b32 %3, %7;"
-                 : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w)
-                 : "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
-    unpack2<T>(c, o);
+    unpack2<T>(make_uint4(v.x | z, v.y | z, v.z | z, v.w | z), o);
   }
+}
+
+__device__ __forceinline__ uint4 ld_shared_v4_dep(const void* p, uint32_t z) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p)) + z));
+  return v;
 }
 
 template <typename T>
