@@ -36,7 +36,7 @@ Tuning g_tune[2];
 std::mutex g_mu;
 
 constexpr int kSmemOptin = 227 * 1024;  // sm_100 per-CTA opt-in maximum
-constexpr int kDefaultBudget[2] = {100 * 1024, 200 * 1024};
+constexpr int kDefaultBudget[2] = {100 * 1024, 150 * 1024};
 constexpr int kDefaultR[2] = {2, 2};
 
 // ---------------------------------------------------------------- device info
@@ -288,7 +288,7 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
       pl.threads = 256;
       pl.smem = 2 * static_cast<size_t>(D) * cs;
       // variant 1 = keep packed (re-expand per pass), 2 = compiler's choice; default by width
-      const bool repack = tu.variant == 1;
+      const bool repack = tu.variant != 2;
       pl.R = repack ? 1 : 0;
       pl.fn = rows_kernel(dtype, vi, repack);
     } else if (ring_plan(kernel, nvec, row_bytes, cs, tu, &pl)) {
