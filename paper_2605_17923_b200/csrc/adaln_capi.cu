@@ -170,9 +170,10 @@ const void* generic_kernel(int kernel, int dtype) {
     return kernel ? (const void*)t.bwd_generic : (const void*)t.fwd_generic;
   });
 }
-const void* reduce_kernel(int dtype) {
-  return dtype == AL_F64 ? (const void*)al::adaln_bwd_reduce<double>
-                         : (const void*)al::adaln_bwd_reduce<float>;
+const void* reduce_kernel(int dtype, bool vec) {
+  if (dtype == AL_F64)
+    return vec ? (const void*)al::adaln_bwd_reduce_vec<double> : (const void*)al::adaln_bwd_reduce<double>;
+  return vec ? (const void*)al::adaln_bwd_reduce_vec<float> : (const void*)al::adaln_bwd_reduce<float>;
 }
 
 // Per-(kernel image, device) one-time attribute setup.
@@ -385,9 +386,11 @@ int al_device_init(int device) {
       e = cudaFuncGetAttributes(&fa, generic_kernel(kernel, dt));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
     }
-    cudaFuncAttributes fa;
-    e = cudaFuncGetAttributes(&fa, reduce_kernel(dt));
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+    for (bool vec : {false, true}) {
+      cudaFuncAttributes fa;
+      e = cudaFuncGetAttributes(&fa, reduce_kernel(dt, vec));
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+    }
   }
   return AL_OK;
 }
@@ -520,10 +523,15 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   void* args[] = {&p};
   cudaError_t e = cudaLaunchKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "backward stage-1 launch");
-  const void* rk = reduce_kernel(dtype);
+  // stage 2: 16-byte vector form when every partial row is 16-byte aligned
+  const int cs = ct_size(dtype);
+  const bool vec = (dim * cs) % 16 == 0 && aligned16(workspace);
+  const void* rk = reduce_kernel(dtype, vec);
   int64_t G64 = pl.grid;
   void* rargs[] = {&workspace, &dscale, &dshift, &p.N, &p.S_grp, &p.D, &G64, &p.nslots};
-  dim3 rgrid(static_cast<unsigned>((dim + 31) / 32), static_cast<unsigned>(ngroups));
+  const int64_t cols_per_cta = vec ? 16 * (16 / cs) : 32;
+  dim3 rgrid(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
+             static_cast<unsigned>(ngroups));
   e = cudaLaunchKernel(rk, rgrid, dim3(1024), rargs, 0, st);
   if (e != cudaSuccess) return cuda_fail(e, "backward stage-2 launch");
   return AL_OK;

@@ -646,7 +646,8 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
     for (int rr = 0; rr < R; ++rr) {
       const bool live = rr < rows;
       const P nm = splat2(-mcur[rr]), r2 = splat2(rcur[rr]);
-      P sg = splat2(CT(0)), sgx = splat2(CT(0));
+      // two accumulators per row sum break the FADD2/FFMA2 dependency chains
+      P sg[2] = {splat2(CT(0)), splat2(CT(0))}, sgx[2] = {splat2(CT(0)), splat2(CT(0))};
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         const bool ok = live && (vmask >> j & 1);
@@ -657,14 +658,15 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
         for (int e = 0; e < NP; ++e) {
           xh[rr][j][e] = mul2(add2(xv[e], nm), r2);
           gg[rr][j][e] = mul2(dv[e], s1[j][e]);
-          sg = add2(sg, gg[rr][j][e]);
-          sgx = fma2(gg[rr][j][e], xh[rr][j][e], sgx);
+          sg[e & 1] = add2(sg[e & 1], gg[rr][j][e]);
+          sgx[e & 1] = fma2(gg[rr][j][e], xh[rr][j][e], sgx[e & 1]);
           acc_sh[j][e] = add2(acc_sh[j][e], dv[e]);
           acc_sc[j][e] = fma2(dv[e], xh[rr][j][e], acc_sc[j][e]);
         }
       }
-      rowsum[2 * rr] = sg.x + sg.y;
-      rowsum[2 * rr + 1] = sgx.x + sgx.y;
+      const P tsg = add2(sg[0], sg[1]), tsgx = add2(sgx[0], sgx[1]);
+      rowsum[2 * rr] = tsg.x + tsg.y;
+      rowsum[2 * rr + 1] = tsgx.x + tsgx.y;
     }
 #pragma unroll
     for (int q = 0; q < 2 * R; ++q) rowsum[q] = warp_sum(rowsum[q]);
@@ -725,9 +727,88 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
 
 // =====================================================================================
 // Backward stage 2: dscale/dshift[g, d] = sum over the CTAs covering group g, ascending.
-// grid = (ceil(D/32), ngroups), block = 1024: 32 columns x 32 slot lanes; each thread keeps
-// several independent loads in flight, then the 32 slot lanes are combined in a fixed order.
+// Vector form (D a multiple of 16 B of partials): block = 1024 threads = 16 column vectors
+// (64 fp32 / 32 fp64 columns) x 64 slot lanes; each thread issues all of its 16-byte loads
+// before adding, the two half-warps of a warp are combined by a shuffle and the 32 warps in
+// ascending order through shared memory -- a fixed order, so the result is deterministic.
 // =====================================================================================
+template <typename CT>
+__global__ void __launch_bounds__(1024) adaln_bwd_reduce_vec(const CT* __restrict__ ws,
+                                                             CT* __restrict__ dscale,
+                                                             CT* __restrict__ dshift, int64_t N,
+                                                             int64_t S_grp, int64_t D, int64_t G,
+                                                             int64_t nslots) {
+  constexpr int VE = 16 / sizeof(CT);  // columns per 16-byte vector
+  constexpr int COLS = 16 * VE;        // columns per CTA
+  __shared__ double part[2][32][COLS + 1];
+  const int t = threadIdx.x, hl = t & 15, sl = t >> 4, warp = t >> 5;
+  const int64_t g = blockIdx.y;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * COLS + hl * VE;
+  const int64_t first_row = g * S_grp;
+  const int64_t last_row = ((g + 1) * S_grp < N ? (g + 1) * S_grp : N) - 1;
+  const int64_t kf = part_owner(first_row, N, G), kl = part_owner(last_row, N, G);
+  const int64_t n = kl - kf + 1;
+  double a[VE], b[VE];
+#pragma unroll
+  for (int e = 0; e < VE; ++e) a[e] = b[e] = 0.0;
+  if (col < D) {
+    const CT* sc = ws + (kf + g) * D + col;
+    const CT* sh = ws + (nslots + kf + g) * D + col;
+    int64_t i = sl;
+    for (; i + 192 < n; i += 256) {  // 4 slots x 2 arrays of 16-byte loads in flight
+      uint4 va[4], vb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        va[u] = __ldg(reinterpret_cast<const uint4*>(sc + (i + 64 * u) * D));
+        vb[u] = __ldg(reinterpret_cast<const uint4*>(sh + (i + 64 * u) * D));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const CT* pa = reinterpret_cast<const CT*>(&va[u]);
+        const CT* pb = reinterpret_cast<const CT*>(&vb[u]);
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+          a[e] += static_cast<double>(pa[e]);
+          b[e] += static_cast<double>(pb[e]);
+        }
+      }
+    }
+    for (; i < n; i += 64) {
+      const uint4 va = __ldg(reinterpret_cast<const uint4*>(sc + i * D));
+      const uint4 vb = __ldg(reinterpret_cast<const uint4*>(sh + i * D));
+      const CT* pa = reinterpret_cast<const CT*>(&va);
+      const CT* pb = reinterpret_cast<const CT*>(&vb);
+#pragma unroll
+      for (int e = 0; e < VE; ++e) {
+        a[e] += static_cast<double>(pa[e]);
+        b[e] += static_cast<double>(pb[e]);
+      }
+    }
+  }
+  // half-warp (slot lanes 2w, 2w+1) combine, fixed order: lower half + upper half
+#pragma unroll
+  for (int e = 0; e < VE; ++e) {
+    const double ua = __shfl_down_sync(0xffffffffu, a[e], 16);
+    const double ub = __shfl_down_sync(0xffffffffu, b[e], 16);
+    if ((t & 31) < 16) {
+      part[0][warp][hl * VE + e] = a[e] + ua;
+      part[1][warp][hl * VE + e] = b[e] + ub;
+    }
+  }
+  __syncthreads();
+  if (t < 2 * COLS) {
+    const int which = t / COLS, c = t % COLS;
+    const int64_t oc = static_cast<int64_t>(blockIdx.x) * COLS + c;
+    if (oc < D) {
+      double s = 0.0;
+#pragma unroll 8
+      for (int q = 0; q < 32; ++q) s += part[which][q][c];
+      (which == 0 ? dscale : dshift)[g * D + oc] = static_cast<CT>(s);
+    }
+  }
+}
+
+// Scalar form for any D: block = 1024 threads = 32 columns x 32 slot lanes.
 template <typename CT>
 __global__ void __launch_bounds__(1024) adaln_bwd_reduce(const CT* __restrict__ ws,
                                                          CT* __restrict__ dscale,
@@ -745,21 +826,7 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce(const CT* __restrict__ 
   if (col < D) {
     const CT* sc = ws + (kf + g) * D + col;
     const CT* sh = ws + (nslots + kf + g) * D + col;
-    const int64_t n = kl - kf + 1;
-    int64_t i = w;
-    for (; i + 96 < n; i += 128) {
-      const CT a0 = sc[i * D], a1 = sc[(i + 32) * D], a2 = sc[(i + 64) * D], a3 = sc[(i + 96) * D];
-      const CT b0 = sh[i * D], b1 = sh[(i + 32) * D], b2 = sh[(i + 64) * D], b3 = sh[(i + 96) * D];
-      a += static_cast<double>(a0);
-      a += static_cast<double>(a1);
-      a += static_cast<double>(a2);
-      a += static_cast<double>(a3);
-      b += static_cast<double>(b0);
-      b += static_cast<double>(b1);
-      b += static_cast<double>(b2);
-      b += static_cast<double>(b3);
-    }
-    for (; i < n; i += 32) {
+    for (int64_t i = w; i <= kl - kf; i += 32) {
       a += static_cast<double>(sc[i * D]);
       b += static_cast<double>(sh[i * D]);
     }
