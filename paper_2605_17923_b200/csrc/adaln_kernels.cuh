@@ -232,28 +232,10 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
         if (c < p.nvec) {
           P q[NP], a[NP], b[NP];
           expand(v[i], z2, q);
-          if constexpr (PACKED) {
-            // modulation pairs read after the statistic is known (no early hoisting)
 #pragma unroll
-            for (int e = 0; e < NP; e += 2) {
-              const uint4 ua = ld_shared_v4_dep(&s1[c * NP + e], z2);
-              const uint4 ub = ld_shared_v4_dep(&sh[c * NP + e], z2);
-              if constexpr (sizeof(CT) == 4) {
-                a[e] = make_float2(__uint_as_float(ua.x), __uint_as_float(ua.y));
-                a[e + 1] = make_float2(__uint_as_float(ua.z), __uint_as_float(ua.w));
-                b[e] = make_float2(__uint_as_float(ub.x), __uint_as_float(ub.y));
-                b[e + 1] = make_float2(__uint_as_float(ub.z), __uint_as_float(ub.w));
-              } else {
-                unpack2<double>(ua, &a[e]);
-                unpack2<double>(ub, &b[e]);
-              }
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < NP; ++e) {
-              a[e] = s1[c * NP + e];
-              b[e] = sh[c * NP + e];
-            }
+          for (int e = 0; e < NP; ++e) {
+            a[e] = s1[c * NP + e];
+            b[e] = sh[c * NP + e];
           }
 #pragma unroll
           for (int e = 0; e < NP; ++e) {

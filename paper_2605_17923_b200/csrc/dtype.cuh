@@ -179,7 +179,8 @@ __device__ __forceinline__ void unpack2<__half>(const uint4& v, float2* o) {
 }
 
 // Same as unpack2, but each expansion carries a true data dependency on `z`, a runtime zero
-// derived from a per-row statistic: ptxas cannot hoist the expansion ahead of that statistic,
+// derived from a per-row statistic (1 only if the statistic is NaN, in which case the row's
+// outputs are NaN regardless): ptxas cannot hoist the expansion ahead of that statistic,
 // so a register-resident row stays packed between passes instead of living unpacked
 // (bf16: PRMT against z; other types: OR with z).
 __device__ __forceinline__ uint32_t runtime_zero(float stat) {
@@ -208,14 +209,6 @@ __device__ __forceinline__ void unpack2_dep(const uint4& v, uint32_t z,
   } else {
     unpack2<T>(make_uint4(v.x | z, v.y | z, v.z | z, v.w | z), o);
   }
-}
-
-__device__ __forceinline__ uint4 ld_shared_v4_dep(const void* p, uint32_t z) {
-  uint4 v;
-  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-      : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p)) + z));
-  return v;
 }
 
 template <typename T>
