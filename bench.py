@@ -387,7 +387,12 @@ def main():
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup(args)
     try:
-        if args.workload == "dit":
+        if args.workload == "dit" and args.impl == "reference":
+            if rank == 0:
+                print(json.dumps({"impl": "reference", "unavailable":
+                                  "the reference has no DiT step: its DP step is a simulated "
+                                  "barrier (cluster_sim.py:134-158)"}), flush=True)
+        elif args.workload == "dit":
             from paper_2605_17923_b200 import dp_step
 
             dp_step.bench_main(args, rest, world, rank, local)

@@ -1,0 +1,281 @@
+"""Data-parallel DiT-block training step fed by the bucket sampler (north-star subsystem 3).
+
+The reference has no GPU step: it models the data-parallel barrier as T_sync = max_i T_i
+(cluster_sim.py:134-158) over synthetic times.  This module runs the real thing on B200s:
+
+* every rank builds the same ``BucketSampler`` (same seed) and takes shard ``rank`` of each
+  step's draw -- bucket assignment needs no communication and is bit-identical to the
+  reference's ``sample_assignments`` (cluster_sim.py:113-131);
+* rank i runs forward + backward of a Wan-2.1-style DiT block on its synthetic batch
+  [B_i, S_i, D] (fused AdaLN from ``adaln.FusedAdaLNModulate`` for both modulated norms;
+  attention/GEMMs through torch, i.e. cuBLAS / flash SDPA);
+* the only collective is ONE NCCL all-reduce of the flat fp32 gradient buffer at the step
+  boundary (NVLink / NVSwitch), then a fused AdamW step;
+* the per-rank compute time T_i (CUDA events, before the all-reduce) is all-gathered (a few
+  bytes) to report the reference's imbalance metrics on measured times: cv_step = (max-min)/max
+  (cluster_sim.py:161-166) and wait_sync = max T - T_i, next to compute_cv over B_i * S_i^2
+  (cluster_sim.py:169-174).
+
+Gradient averaging with heterogeneous per-rank batches is token-weighted: each rank's loss is
+the sum of its per-token losses divided by the step's GLOBAL token count (known on every rank
+from the shared draw), so the all-reduce SUM is exactly the global per-token mean gradient.
+
+The block (Wan-2.1-1.3B widths: D=1536, 12 heads, FFN 8960) is public architecture, not part
+of the reference; weights are random-initialised and the data synthetic.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+from .sampler import BucketSampler, RankShard, compute_cv, cv_step
+from .scheduler import emit_plan
+
+__all__ = ["WanStyleBlock", "DPStepRunner", "StepStats", "bench_main"]
+
+
+@dataclass(frozen=True)
+class BlockConfig:
+    dim: int = 1536
+    heads: int = 12
+    ffn: int = 8960
+    eps: float = 1e-6
+
+
+class WanStyleBlock(nn.Module):
+    """AdaLN-modulated self-attention + FFN block with six per-sample modulation vectors.
+
+    ``norm_fn(x, scale, shift, eps)`` is the fused LayerNorm-Modulate; the default is the
+    sm_100a kernel pair (``adaln_modulate``).  Tests may inject a CPU stand-in to exercise the
+    data-parallel host logic on gloo.
+    """
+
+    def __init__(self, cfg: BlockConfig = BlockConfig(), norm_fn=None):
+        super().__init__()
+        self.cfg = cfg
+        d = cfg.dim
+        self.modulation = nn.Parameter(torch.randn(1, 6, d) / math.sqrt(d))
+        self.time_proj = nn.Linear(d, 6 * d)
+        self.qkv = nn.Linear(d, 3 * d)
+        self.q_norm = nn.RMSNorm(d // cfg.heads, eps=cfg.eps)
+        self.k_norm = nn.RMSNorm(d // cfg.heads, eps=cfg.eps)
+        self.proj = nn.Linear(d, d)
+        self.ffn_in = nn.Linear(d, cfg.ffn)
+        self.ffn_out = nn.Linear(cfg.ffn, d)
+        if norm_fn is None:
+            from .adaln import adaln_modulate
+
+            norm_fn = adaln_modulate
+        self.norm_fn = norm_fn
+
+    def forward(self, x: torch.Tensor, t_emb: torch.Tensor) -> torch.Tensor:
+        b, s, d = x.shape
+        h = self.cfg.heads
+        e = (self.time_proj(F.silu(t_emb)).view(b, 6, d) + self.modulation).to(x.dtype)
+        shift1, scale1, gate1, shift2, scale2, gate2 = e.unbind(1)
+        y = self.norm_fn(x, scale1.contiguous(), shift1.contiguous(), self.cfg.eps)
+        q, k, v = self.qkv(y).view(b, s, 3, h, d // h).unbind(2)
+        q = self.q_norm(q).to(v.dtype).transpose(1, 2)
+        k = self.k_norm(k).to(v.dtype).transpose(1, 2)
+        v = v.transpose(1, 2)
+        a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(b, s, d)
+        x = x + self.proj(a) * gate1[:, None, :]
+        y = self.norm_fn(x, scale2.contiguous(), shift2.contiguous(), self.cfg.eps)
+        x = x + self.ffn_out(F.gelu(self.ffn_in(y), approximate="tanh")) * gate2[:, None, :]
+        return x
+
+
+@dataclass
+class StepStats:
+    step: int
+    shards: list
+    t_compute_ms: list      # measured T_i per rank (fwd+bwd, before the all-reduce)
+    t_step_ms: float        # max over ranks of the full step (incl. all-reduce + optimizer)
+    tokens: int             # sum of B_i * S_i
+    loads: list             # B_i * S_i^2
+    cv_step: float          # (max - min) / max over measured T_i
+    compute_cv: float       # 100 * std / mean over B_i * S_i^2
+    wait_sync_ms: list      # max T - T_i
+
+    def to_json(self) -> dict:
+        return {"step": self.step, "seq": [sh.seq_len for sh in self.shards],
+                "batch": [sh.batch_size for sh in self.shards],
+                "t_compute_ms": [round(t, 4) for t in self.t_compute_ms],
+                "t_step_ms": round(self.t_step_ms, 4), "tokens": self.tokens,
+                "cv_step": self.cv_step, "compute_cv": self.compute_cv}
+
+
+class DPStepRunner:
+    """One DP rank: shard -> synthetic batch -> fwd/bwd -> one flat all-reduce -> AdamW."""
+
+    def __init__(self, block: nn.Module, device: torch.device, world: int, rank: int,
+                 dtype=torch.bfloat16, lr: float = 1e-4, seed: int = 0, group=None):
+        self.block = block.to(device)
+        self.device = device
+        self.world, self.rank = world, rank
+        self.dtype = dtype
+        self.group = group
+        self.params = [p for p in self.block.parameters() if p.requires_grad]
+        numel = sum(p.numel() for p in self.params)
+        # one contiguous fp32 gradient buffer: the all-reduce is a single NCCL call
+        self.flat_grad = torch.zeros(numel, dtype=torch.float32, device=device)
+        off = 0
+        for p in self.params:
+            p.grad = self.flat_grad[off:off + p.numel()].view_as(p)
+            off += p.numel()
+        fused = device.type == "cuda"
+        self.opt = torch.optim.AdamW(self.params, lr=lr, fused=fused)
+        self.gen = torch.Generator(device=device).manual_seed(seed * 1000 + rank)
+        self.dim = block.cfg.dim
+
+    def make_batch(self, shard: RankShard):
+        b, s, d = shard.batch_size, shard.seq_len, self.dim
+        x = torch.randn(b, s, d, device=self.device, generator=self.gen, dtype=self.dtype)
+        t = torch.randn(b, d, device=self.device, generator=self.gen, dtype=self.dtype)
+        target = torch.randn(b, s, d, device=self.device, generator=self.gen, dtype=self.dtype)
+        return x, t, target
+
+    def _allreduce(self, t: torch.Tensor):
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(t, group=self.group)
+
+    def _all_gather_scalar(self, v: float) -> list:
+        if self.world == 1:
+            return [v]
+        import torch.distributed as dist
+
+        dev = self.device if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+        outs = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(self.world)]
+        dist.all_gather(outs, torch.tensor([v], dtype=torch.float64, device=dev), group=self.group)
+        return [float(a.item()) for a in outs]
+
+    def step(self, step_idx: int, shards: list, batch=None) -> StepStats:
+        mine = shards[self.rank]
+        global_tokens = sum(sh.tokens for sh in shards)
+        x, t, target = batch if batch is not None else self.make_batch(mine)
+        cuda = self.device.type == "cuda"
+        if cuda:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
+        else:
+            t0 = time.perf_counter()
+        self.flat_grad.zero_()
+        with torch.autocast(self.device.type, dtype=torch.bfloat16, enabled=cuda):
+            out = self.block(x, t)
+            # token-weighted: per-token MSE summed locally, normalised by the GLOBAL token count
+            loss = F.mse_loss(out.float(), target.float(), reduction="sum") / (
+                global_tokens * self.dim)
+        loss.backward()
+        if cuda:
+            ev[1].record()
+        else:
+            t1 = time.perf_counter()
+        self._allreduce(self.flat_grad)
+        self.opt.step()
+        if cuda:
+            ev[2].record()
+            torch.cuda.synchronize(self.device)
+            t_comp = ev[0].elapsed_time(ev[1])
+            t_step = ev[0].elapsed_time(ev[2])
+        else:
+            t_comp = 1e3 * (t1 - t0)
+            t_step = 1e3 * (time.perf_counter() - t0)
+        times = self._all_gather_scalar(t_comp)
+        t_step_max = max(self._all_gather_scalar(t_step))
+        loads = [sh.load for sh in shards]
+        return StepStats(step_idx, shards, times, t_step_max, global_tokens, loads,
+                         cv_step(times), compute_cv(loads) if len(loads) > 1 else 0.0,
+                         [max(times) - v for v in times])
+
+
+def run_policy_steps(runner: DPStepRunner, sampler: BucketSampler, steps: int,
+                     warmup: int = 0) -> list:
+    stats = []
+    for i in range(warmup + steps):
+        shards = sampler.step()
+        st = runner.step(i, shards)
+        if i >= warmup:
+            stats.append(st)
+    return stats
+
+
+def summarize(stats: list, world: int) -> dict:
+    tok = sum(s.tokens for s in stats)
+    t = sum(s.t_step_ms for s in stats) / 1e3
+    return {
+        "steps": len(stats),
+        "tokens_per_sec": tok / t if t > 0 else 0.0,
+        "mean_step_ms": 1e3 * t / max(len(stats), 1),
+        "mean_cv_step_measured": float(np.mean([s.cv_step for s in stats])) if world > 1 else 0.0,
+        "mean_compute_cv": float(np.mean([s.compute_cv for s in stats])) if world > 1 else 0.0,
+        "mean_wait_sync_ms": float(np.mean([np.mean(s.wait_sync_ms) for s in stats])),
+    }
+
+
+# ------------------------------------------------------------------------------ bench entry
+def bench_main(args, rest, world: int, rank: int, local: int) -> None:
+    """``bench.py --workload dit``: tokens/s of the balanced step at N GPUs (dual-constraint
+    plan) next to the equal-token baseline, with measured and load imbalance."""
+    import argparse
+
+    from .catalogs import reference_default_catalog
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--policy-steps", type=int, default=0)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--token-budget", type=int, default=480_000)
+    ap.add_argument("--m-comp", type=float, default=0.0)
+    extra = ap.parse_args(rest)
+    dev = torch.device("cuda", local)
+    catalog, weights, tb, dc = reference_default_catalog()
+    # the reference's defaults (480k-token envelope, M_comp = 3e9, p = 2: cluster_sim.py:328-336);
+    # a different --token-budget scales M_comp to keep the reference's M_comp / M_mem^2
+    m_mem = extra.token_budget
+    m_comp = extra.m_comp or dc.m_comp * (m_mem / dc.m_mem) ** 2
+    from .scheduler import DualConstraint, TokenBudget
+
+    plan_a = emit_plan(catalog, TokenBudget(m_mem))
+    plan_b = emit_plan(catalog, DualConstraint(float(m_mem), m_comp, 2.0))
+    steps = extra.policy_steps or args.steps
+    out = {}
+    for name, plan in (("equal_token", plan_a), ("dual", plan_b)):
+        torch.manual_seed(0)
+        runner = DPStepRunner(WanStyleBlock(), dev, world, rank, seed=extra.seed)
+        sampler = BucketSampler(catalog, weights, plan, max(world, 1), extra.seed)
+        stats = run_policy_steps(runner, sampler, steps, warmup=args.warmup)
+        out[name] = summarize(stats, world)
+        del runner
+        torch.cuda.empty_cache()
+    if rank == 0:
+        line = {
+            "metric": "DiT-block DP step tokens/s (dual-constraint buckets)",
+            "value": round(out["dual"]["tokens_per_sec"], 1), "unit": "tokens/s",
+            "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": round(out["dual"]["mean_step_ms"], 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "Wan-2.1-1.3B-style block (D=1536, 12 heads, FFN 8960), fused "
+                                   "AdaLN x2, reference default catalog, per-rank draws",
+                       "token_budget": m_mem, "m_comp": m_comp, "p": 2.0,
+                       "parallelism": f"dp{world}, one NCCL all-reduce per step"},
+            "policies": out,
+            "imbalance": {
+                "compute_cv_equal_token_pct": out["equal_token"]["mean_compute_cv"],
+                "compute_cv_dual_pct": out["dual"]["mean_compute_cv"],
+                "cv_step_measured_equal_token": out["equal_token"]["mean_cv_step_measured"],
+                "cv_step_measured_dual": out["dual"]["mean_cv_step_measured"],
+            },
+            "throughput_gain_vs_equal_token": (out["dual"]["tokens_per_sec"]
+                                               / max(out["equal_token"]["tokens_per_sec"], 1e-9)
+                                               - 1.0),
+        }
+        print(json.dumps(line), flush=True)
