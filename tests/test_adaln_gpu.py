@@ -485,3 +485,25 @@ def test_cuda_graph_capture(cuda):
     assert torch.equal(y, y0) and torch.equal(mu, mu0)
     for a, b in zip(d, d0):
         assert torch.equal(a, b)
+
+
+# ------------------------------------------------------------------ reference backend protocol
+def test_reference_backend_protocol(adaln_golden, cuda):
+    """The four-function module the reference's _select_backend loads, served by the GPU."""
+    from paper_2605_17923_b200.adaln import reference_backend as be
+
+    g = adaln_golden
+    for c in _golden_cases(g):
+        p = c + "/"
+        x, sc, sh, dy, eps = g[p + "x"], g[p + "scale"], g[p + "shift"], g[p + "dy"], float(g[p + "eps"])
+        y, mu, rstd = be.forward(x, sc, sh, eps)
+        assert max_rel_err(y, g[p + "y"]) <= 1e-12, c
+        dx, dsc, dsh = be.backward_naive(dy, x, sc, g[p + "mu"], g[p + "rstd"])
+        assert np.abs(dx - g[p + "dx"]).max() <= 1e-12 * max(1.0, np.abs(g[p + "dx"]).max()), c
+        assert max_rel_err(dsc, g[p + "dscale"]) <= 1e-12, c
+        assert np.array_equal(be.backward_dx(dy, x, sc, g[p + "mu"], g[p + "rstd"]), dx)
+        for dt, nt in g[p + "tiles"]:
+            a, b = be.dtile_reduce(dy, x, g[p + "mu"], g[p + "rstd"], int(dt), int(nt), False)
+            q = f"{p}dtile_{dt}_{nt}_0/"
+            assert max_rel_err(a, g[q + "dscale"]) <= 1e-12, (c, dt, nt)
+            assert max_rel_err(b, g[q + "dshift"]) <= 1e-12, (c, dt, nt)
