@@ -198,6 +198,51 @@ class DPStepRunner:
                          [max(times) - v for v in times])
 
 
+def measure_trials(runner: DPStepRunner, requests, reps: int = 3) -> list:
+    """Time one rank's fwd+bwd for each (B, S) request (CUDA events, median of `reps` after a
+    warm-up); returns costfit.Trial records in seconds -- the B200 counterpart of the
+    reference's synthetic sweep (costfit.generate_sweep + cluster_sim ground truth)."""
+    from .costfit import Trial
+    from .shapes import Bucket, MediaShape
+
+    out = []
+    for b, s in requests:
+        shard = RankShard(runner.rank, -1, Bucket(MediaShape(1, 16, 16), s, 1), b)
+        batch = runner.make_batch(shard)
+        times = []
+        for _ in range(reps + 1):
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            runner.flat_grad.zero_()
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                o = runner.block(batch[0], batch[1])
+                loss = F.mse_loss(o.float(), batch[2].float())
+            loss.backward()
+            ev1.record()
+            torch.cuda.synchronize(runner.device)
+            times.append(ev0.elapsed_time(ev1) / 1e3)
+        out.append(Trial(b, s, float(np.median(times[1:]))))
+        del batch, o, loss
+    return out
+
+
+def calibrate_plan(runner: DPStepRunner, catalog, m_mem: float, grid=None):
+    """Sweep -> fit T = a + b B S^p -> dual constraint planning every bucket to the longest
+    bucket's B=1 time.  Returns (plan, model, trials)."""
+    from .costfit import GridSpec, calibrated_dual_constraint, fit_cost_model, generate_sweep
+
+    reqs = list(generate_sweep(catalog).trials)
+    # also measure each bucket at its memory envelope, the regime the plans actually run in
+    for bucket in catalog:
+        b_env = max(1, int(m_mem // bucket.seq_len))
+        if (b_env, bucket.seq_len) not in reqs:
+            reqs.append((b_env, bucket.seq_len))
+    trials = measure_trials(runner, reqs)
+    model = fit_cost_model(trials, grid or GridSpec(1.0, 2.4, 0.05))
+    dc = calibrated_dual_constraint(model, catalog, m_mem)
+    return emit_plan(catalog, dc), model, trials
+
+
 def run_policy_steps(runner: DPStepRunner, sampler: BucketSampler, steps: int,
                      warmup: int = 0) -> list:
     stats = []
@@ -235,6 +280,7 @@ def bench_main(args, rest, world: int, rank: int, local: int) -> None:
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--token-budget", type=int, default=480_000)
     ap.add_argument("--m-comp", type=float, default=0.0)
+    ap.add_argument("--plan", choices=["calibrated", "reference"], default="calibrated")
     extra = ap.parse_args(rest)
     dev = torch.device("cuda", local)
     catalog, weights, tb, dc = reference_default_catalog()
@@ -246,6 +292,28 @@ def bench_main(args, rest, world: int, rank: int, local: int) -> None:
 
     plan_a = emit_plan(catalog, TokenBudget(m_mem))
     plan_b = emit_plan(catalog, DualConstraint(float(m_mem), m_comp, 2.0))
+    calib = None
+    if extra.plan == "calibrated":
+        # every rank measures and fits on its own GPU; rank 0's fit is broadcast so all ranks
+        # plan identically (the plan must be common to keep the draws rank-consistent)
+        torch.manual_seed(0)
+        cal_runner = DPStepRunner(WanStyleBlock(), dev, 1, 0, seed=extra.seed)
+        plan_b, model, trials = calibrate_plan(cal_runner, catalog, m_mem)
+        vec = torch.tensor([model.a, model.b, model.p, model.r2], dtype=torch.float64, device=dev)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.broadcast(vec, 0)
+        from .costfit import CostModel, calibrated_dual_constraint
+
+        model = CostModel(*[float(v) for v in vec.cpu()])
+        dc_cal = calibrated_dual_constraint(model, catalog, m_mem)
+        plan_b = emit_plan(catalog, dc_cal)
+        calib = {"a": model.a, "b": model.b, "p": model.p, "r2": model.r2,
+                 "m_comp": dc_cal.m_comp,
+                 "trials": [[t.batch, t.seq_len, round(t.step_time, 6)] for t in trials]}
+        del cal_runner
+        torch.cuda.empty_cache()
     steps = extra.policy_steps or args.steps
     out = {}
     for name, plan in (("equal_token", plan_a), ("dual", plan_b)):
@@ -265,9 +333,12 @@ def bench_main(args, rest, world: int, rank: int, local: int) -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "Wan-2.1-1.3B-style block (D=1536, 12 heads, FFN 8960), fused "
                                    "AdaLN x2, reference default catalog, per-rank draws",
-                       "token_budget": m_mem, "m_comp": m_comp, "p": 2.0,
+                       "token_budget": m_mem, "plan": extra.plan,
+                       "plan_equal_token": plan_a.batch_sizes(),
+                       "plan_dual": plan_b.batch_sizes(),
                        "parallelism": f"dp{world}, one NCCL all-reduce per step"},
             "policies": out,
+            "calibration": calib,
             "imbalance": {
                 "compute_cv_equal_token_pct": out["equal_token"]["mean_compute_cv"],
                 "compute_cv_dual_pct": out["dual"]["mean_compute_cv"],

@@ -202,7 +202,37 @@ def make_sampler():
                     for s in shapes if (s[0] - 1) % 8 == 0],
         "lambda4": [[*s, sequence_length(MediaShape(*s), geom4)] for s in shapes],
     }
+    out["costfit"] = make_costfit()
     (OUT / "sampler_golden.json").write_text(json.dumps(out, indent=1, sort_keys=True))
+
+
+def make_costfit():
+    from adaptiveload.costfit import (GridSpec, Trial, correlation_report, derive_m_comp,
+                                      fit_cost_model, generate_sweep)
+
+    res = {"recovery": [], "grids": {}}
+    pairs = [(bb, ss) for bb in (1, 2, 3) for ss in (8000, 24000, 48000)]
+    for p_true in GridSpec().values():  # test_acceptance.py:69-83 (criterion 3)
+        trials = [Trial(b, s, 2.0 + 1e-9 * b * float(s) ** p_true) for b, s in pairs]
+        m = fit_cost_model(trials)
+        res["recovery"].append({"trials": [[t.batch, t.seq_len, t.step_time] for t in trials],
+                                "fit": [m.a, m.b, m.p, m.r2],
+                                "m_comp_62": derive_m_comp(m, 62.0)})
+    rng = np.random.default_rng(7)
+    noisy = []
+    for _ in range(100):
+        b = int(rng.integers(1, 5))
+        s = int(rng.choice([1600, 4800, 9600, 24000, 48000, 52800]))
+        noisy.append(Trial(b, s, float((2.0 + 1e-9 * b * s**2) * (1 + rng.normal(0, 0.05)))))
+    m = fit_cost_model(noisy)
+    res["noisy"] = {"trials": [[t.batch, t.seq_len, t.step_time] for t in noisy],
+                    "fit": [m.a, m.b, m.p, m.r2], "corr": correlation_report(noisy, 2.0)}
+    wide = GridSpec(1.0, 2.4, 0.05)
+    m = fit_cost_model(noisy, wide)
+    res["grids"]["wide"] = {"values": wide.values(), "fit": [m.a, m.b, m.p, m.r2]}
+    cat, _ = default_catalog()
+    res["sweep_default"] = [list(r) for r in generate_sweep(cat).trials]
+    return res
 
 
 if __name__ == "__main__":
