@@ -226,10 +226,14 @@ def measure_trials(runner: DPStepRunner, requests, reps: int = 3) -> list:
     return out
 
 
-def calibrate_plan(runner: DPStepRunner, catalog, m_mem: float, grid=None):
-    """Sweep -> fit T = a + b B S^p -> dual constraint planning every bucket to the longest
-    bucket's B=1 time.  Returns (plan, model, trials)."""
-    from .costfit import GridSpec, calibrated_dual_constraint, fit_cost_model, generate_sweep
+def calibrate_plan(runner: DPStepRunner, catalog, m_mem: float, cost_model: str = "quadratic"):
+    """Sweep -> fit -> plan every bucket to the longest bucket's B=1 time.
+
+    cost_model "power": the reference's T = a + b B S^p (grid-searched p) and its dual
+    constraint; "quadratic": T = a + c1 B S + c2 B S^2 (costfit.time_balanced_plan).
+    Returns (plan, fits, trials)."""
+    from .costfit import (GridSpec, calibrated_dual_constraint, fit_cost_model,
+                          fit_quadratic_cost_model, generate_sweep)
 
     reqs = list(generate_sweep(catalog).trials)
     # also measure each bucket at its memory envelope, the regime the plans actually run in
@@ -238,9 +242,17 @@ def calibrate_plan(runner: DPStepRunner, catalog, m_mem: float, grid=None):
         if (b_env, bucket.seq_len) not in reqs:
             reqs.append((b_env, bucket.seq_len))
     trials = measure_trials(runner, reqs)
-    model = fit_cost_model(trials, grid or GridSpec(1.0, 2.4, 0.05))
-    dc = calibrated_dual_constraint(model, catalog, m_mem)
-    return emit_plan(catalog, dc), model, trials
+    fits = {"power": fit_cost_model(trials, GridSpec(1.0, 2.4, 0.05)),
+            "quadratic": fit_quadratic_cost_model(trials)}
+    return fits, trials
+
+
+def plan_from_fit(kind: str, model, catalog, m_mem: float):
+    from .costfit import calibrated_dual_constraint, time_balanced_plan
+
+    if kind == "power":
+        return emit_plan(catalog, calibrated_dual_constraint(model, catalog, m_mem))
+    return time_balanced_plan(model, catalog, m_mem)
 
 
 def run_policy_steps(runner: DPStepRunner, sampler: BucketSampler, steps: int,
@@ -281,6 +293,7 @@ def bench_main(args, rest, world: int, rank: int, local: int) -> None:
     ap.add_argument("--token-budget", type=int, default=480_000)
     ap.add_argument("--m-comp", type=float, default=0.0)
     ap.add_argument("--plan", choices=["calibrated", "reference"], default="calibrated")
+    ap.add_argument("--cost-model", choices=["quadratic", "power"], default="quadratic")
     extra = ap.parse_args(rest)
     dev = torch.device("cuda", local)
     catalog, weights, tb, dc = reference_default_catalog()
@@ -294,26 +307,34 @@ def bench_main(args, rest, world: int, rank: int, local: int) -> None:
     plan_b = emit_plan(catalog, DualConstraint(float(m_mem), m_comp, 2.0))
     calib = None
     if extra.plan == "calibrated":
-        # every rank measures and fits on its own GPU; rank 0's fit is broadcast so all ranks
-        # plan identically (the plan must be common to keep the draws rank-consistent)
-        torch.manual_seed(0)
-        cal_runner = DPStepRunner(WanStyleBlock(), dev, 1, 0, seed=extra.seed)
-        plan_b, model, trials = calibrate_plan(cal_runner, catalog, m_mem)
-        vec = torch.tensor([model.a, model.b, model.p, model.r2], dtype=torch.float64, device=dev)
+        # rank 0 measures and fits; the fit is broadcast so every rank plans identically (the
+        # plan must be common for the draws to stay rank-consistent)
+        from .costfit import CostModel, QuadraticCostModel
+
+        vec = torch.zeros(8, dtype=torch.float64, device=dev)
+        trials = []
+        if rank == 0:
+            torch.manual_seed(0)
+            cal_runner = DPStepRunner(WanStyleBlock(), dev, 1, 0, seed=extra.seed)
+            fits, trials = calibrate_plan(cal_runner, catalog, m_mem)
+            pw, qd = fits["power"], fits["quadratic"]
+            vec = torch.tensor([pw.a, pw.b, pw.p, pw.r2, qd.a, qd.c1, qd.c2, qd.r2],
+                               dtype=torch.float64, device=dev)
+            del cal_runner
+            torch.cuda.empty_cache()
         if world > 1:
             import torch.distributed as dist
 
             dist.broadcast(vec, 0)
-        from .costfit import CostModel, calibrated_dual_constraint
-
-        model = CostModel(*[float(v) for v in vec.cpu()])
-        dc_cal = calibrated_dual_constraint(model, catalog, m_mem)
-        plan_b = emit_plan(catalog, dc_cal)
-        calib = {"a": model.a, "b": model.b, "p": model.p, "r2": model.r2,
-                 "m_comp": dc_cal.m_comp,
-                 "trials": [[t.batch, t.seq_len, round(t.step_time, 6)] for t in trials]}
-        del cal_runner
-        torch.cuda.empty_cache()
+        v = [float(a) for a in vec.cpu()]
+        fits = {"power": CostModel(*v[:4]), "quadratic": QuadraticCostModel(*v[4:])}
+        plan_b = plan_from_fit(extra.cost_model, fits[extra.cost_model], catalog, m_mem)
+        calib = {"cost_model": extra.cost_model,
+                 "power_fit": fits["power"].__dict__, "quadratic_fit": fits["quadratic"].__dict__,
+                 "trials": [[t.batch, t.seq_len, round(t.step_time, 6)] for t in trials],
+                 "predicted_ms": [round(1e3 * fits[extra.cost_model].predict(e.batch_size,
+                                                                             e.bucket.seq_len), 3)
+                                  for e in plan_b.entries]}
     steps = extra.policy_steps or args.steps
     out = {}
     for name, plan in (("equal_token", plan_a), ("dual", plan_b)):

@@ -69,3 +69,27 @@ def test_calibrated_plan_equalises_predicted_time():
     for e, t in zip(plan.entries, times):
         if e.binding.value == "compute":
             assert model.predict(e.batch_size + 1, e.bucket.seq_len) > target
+
+
+def test_quadratic_model_fits_measured_b200_block_trials():
+    """Trials measured on a B200 (profiles/r1_dit_calibration.json) -- linear + quadratic."""
+    from paper_2605_17923_b200.costfit import fit_quadratic_cost_model, time_balanced_plan
+
+    rows = [[1, 1600, 0.002236], [2, 1600, 0.002954], [1, 4800, 0.003182], [2, 4800, 0.005478],
+            [1, 9600, 0.006096], [2, 9600, 0.010995], [1, 24000, 0.018733], [2, 24000, 0.03823],
+            [3, 24000, 0.056679], [4, 24000, 0.074578], [1, 48000, 0.058422],
+            [2, 48000, 0.115555], [3, 48000, 0.17569], [4, 48000, 0.235084],
+            [1, 52800, 0.069602], [2, 52800, 0.137786], [3, 52800, 0.210791],
+            [4, 52800, 0.280007], [300, 1600, 0.19181], [100, 4800, 0.219466],
+            [50, 9600, 0.259281], [20, 24000, 0.386167], [10, 48000, 0.59469],
+            [9, 52800, 0.638658]]
+    trials = _trials(rows)
+    q = fit_quadratic_cost_model(trials)
+    pw = fit_cost_model(trials, GridSpec(1.0, 2.4, 0.05))
+    assert q.r2 > 0.999 and q.r2 > pw.r2 and q.c1 > 0 and q.c2 > 0
+    cat, _, _, _ = reference_default_catalog()
+    plan = time_balanced_plan(q, cat, 480_000)
+    pred = [q.predict(e.batch_size, e.bucket.seq_len) for e in plan.entries]
+    target = q.predict(1, 52800)
+    assert max(pred) <= target * (1 + 1e-6)
+    assert plan.batch_sizes() == [110, 32, 13, 3, 1, 1]
