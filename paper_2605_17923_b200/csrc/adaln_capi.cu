@@ -79,6 +79,7 @@ struct Table {
   FwdFn rows_rp[kNumVpl];  // PACKED variant (row kept packed, re-expanded per pass)
   FwdFn wide[3][3];  // [V idx][R idx], V in {1,2,4}, R in {1,2,4}
   BwdFn bwd[3][3];
+  BwdFn bwd_full[3][3];  // nvec == V * consumers: ownership predicates compiled out
   FwdFn fwd_generic;
   BwdFn bwd_generic;
   Table() {
@@ -111,15 +112,24 @@ struct Table {
     wide[2][0] = al::adaln_fwd_wide<T, 4, 1>;
     wide[2][1] = al::adaln_fwd_wide<T, 4, 2>;
     wide[2][2] = al::adaln_fwd_wide<T, 4, 4>;
-    bwd[0][0] = al::adaln_bwd_tma<T, 1, 1>;
-    bwd[0][1] = al::adaln_bwd_tma<T, 1, 2>;
-    bwd[0][2] = al::adaln_bwd_tma<T, 1, 4>;
-    bwd[1][0] = al::adaln_bwd_tma<T, 2, 1>;
-    bwd[1][1] = al::adaln_bwd_tma<T, 2, 2>;
-    bwd[1][2] = al::adaln_bwd_tma<T, 2, 4>;
-    bwd[2][0] = al::adaln_bwd_tma<T, 4, 1>;
-    bwd[2][1] = al::adaln_bwd_tma<T, 4, 2>;
-    bwd[2][2] = al::adaln_bwd_tma<T, 4, 4>;
+    bwd[0][0] = al::adaln_bwd_tma<T, 1, 1, false>;
+    bwd_full[0][0] = al::adaln_bwd_tma<T, 1, 1, true>;
+    bwd[0][1] = al::adaln_bwd_tma<T, 1, 2, false>;
+    bwd_full[0][1] = al::adaln_bwd_tma<T, 1, 2, true>;
+    bwd[0][2] = al::adaln_bwd_tma<T, 1, 4, false>;
+    bwd_full[0][2] = al::adaln_bwd_tma<T, 1, 4, true>;
+    bwd[1][0] = al::adaln_bwd_tma<T, 2, 1, false>;
+    bwd_full[1][0] = al::adaln_bwd_tma<T, 2, 1, true>;
+    bwd[1][1] = al::adaln_bwd_tma<T, 2, 2, false>;
+    bwd_full[1][1] = al::adaln_bwd_tma<T, 2, 2, true>;
+    bwd[1][2] = al::adaln_bwd_tma<T, 2, 4, false>;
+    bwd_full[1][2] = al::adaln_bwd_tma<T, 2, 4, true>;
+    bwd[2][0] = al::adaln_bwd_tma<T, 4, 1, false>;
+    bwd_full[2][0] = al::adaln_bwd_tma<T, 4, 1, true>;
+    bwd[2][1] = al::adaln_bwd_tma<T, 4, 2, false>;
+    bwd_full[2][1] = al::adaln_bwd_tma<T, 4, 2, true>;
+    bwd[2][2] = al::adaln_bwd_tma<T, 4, 4, false>;
+    bwd_full[2][2] = al::adaln_bwd_tma<T, 4, 4, true>;
     fwd_generic = al::adaln_fwd_generic<T>;
     bwd_generic = al::adaln_bwd_generic<T>;
   }
@@ -154,10 +164,11 @@ auto with_table(int dtype, F&& f) {
 }
 
 // path: 1 = TMA ring (wide forward / backward), 2 = rows-in-registers forward
-const void* tma_kernel(int kernel, int dtype, int V, int R) {
+const void* tma_kernel(int kernel, int dtype, int V, int R, bool full = false) {
   const int a = vidx(V), b = vidx(R);
   return with_table(dtype, [&](const auto& t) {
-    return kernel ? (const void*)t.bwd[a][b] : (const void*)t.wide[a][b];
+    if (kernel) return full ? (const void*)t.bwd_full[a][b] : (const void*)t.bwd[a][b];
+    return (const void*)t.wide[a][b];
   });
 }
 const void* rows_kernel(int dtype, int vi, bool repack) {
@@ -293,7 +304,8 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
       pl.R = repack ? 1 : 0;
       pl.fn = rows_kernel(dtype, vi, repack);
     } else if (ring_plan(kernel, nvec, row_bytes, cs, tu, &pl)) {
-      pl.fn = tma_kernel(kernel, dtype, pl.V, pl.R);
+      const bool full = kernel == 1 && nvec == static_cast<int64_t>(pl.V) * (pl.threads - 32);
+      pl.fn = tma_kernel(kernel, dtype, pl.V, pl.R, full);
     }
     if (pl.path != 0) {
       int occ = 0;
@@ -371,10 +383,11 @@ int al_device_init(int device) {
   for (int dt = 0; dt < 4; ++dt) {
     for (int kernel = 0; kernel < 2; ++kernel) {
       for (int V : {1, 2, 4})
-        for (int R : {1, 2, 4}) {
-          rc = ensure_attr(tma_kernel(kernel, dt, V, R), device);
-          if (rc) return rc;
-        }
+        for (int R : {1, 2, 4})
+          for (bool full : {false, true}) {
+            rc = ensure_attr(tma_kernel(kernel, dt, V, R, full), device);
+            if (rc) return rc;
+          }
       if (kernel == 0)
         for (int vi = 0; vi < kNumVpl; ++vi) {
           rc = ensure_attr(rows_kernel(dt, vi, false), device);

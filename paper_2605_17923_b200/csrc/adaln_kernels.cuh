@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(512) adaln_fwd_wide(const FwdParams p) {
 // row-sum barrier, folds dy and dy*xhat into its column accumulators, and after the barrier
 // writes dx = rstd * (g - mean(g) - xhat * mean(g*xhat)).  Packed fp32 pair math.
 // =====================================================================================
-template <typename T, int V, int R>
+template <typename T, int V, int R, bool FULL>
 __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
@@ -527,12 +527,13 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
   }
 
   // ---------------- consumers ----------------
-  uint32_t vmask = 0;
+  // FULL: every consumer owns all V vectors (nvec == V * nc), so ownership tests fold away
+  uint32_t vmask = FULL ? (1u << V) - 1 : 0u;
   int coff[V];  // byte offset of owned vector j inside a row
 #pragma unroll
   for (int j = 0; j < V; ++j) {
     coff[j] = (tid + j * nc) * 16;
-    if (tid + j * nc < p.nvec) vmask |= 1u << j;
+    if (!FULL && tid + j * nc < p.nvec) vmask |= 1u << j;
   }
   const CT invD = CT(1) / static_cast<CT>(p.D);
   const CT* mean_p = static_cast<const CT*>(p.mean);
@@ -650,25 +651,30 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
       rowsum[2 * rr] = tsg.x + tsg.y;
       rowsum[2 * rr + 1] = tsgx.x + tsgx.y;
     }
-#pragma unroll
-    for (int q = 0; q < 2 * R; ++q) rowsum[q] = warp_sum(rowsum[q]);
-    if (lane == 0) {
-#pragma unroll
-      for (int q = 0; q < 2 * R; ++q) rd[warp * 2 * R + q] = rowsum[q];
+    {
+      constexpr int NV = 2 * R, GRP = 32 / NV;
+      const CT u = warp_reduce_scatter<NV>(rowsum, lane);
+      if ((lane & (GRP - 1)) == 0) rd[warp * NV + lane / GRP] = u;
     }
     named_bar_sync(1, nc);
     // every consumer has read this stage into registers: release the slot to the producer
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
-    // cross-warp totals (fixed warp order -> deterministic)
+    // cross-warp totals (fixed warp order -> deterministic), 8/16-byte shared loads
+    P tot2[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) tot2[q] = splat2(CT(0));
+    for (int q = 0; q < ncw; ++q) {
+      const P* src = reinterpret_cast<const P*>(rd + q * 2 * R);
+#pragma unroll
+      for (int u = 0; u < R; ++u) tot2[u] = add2(tot2[u], src[u]);
+    }
     CT tot[2 * R];
 #pragma unroll
-    for (int q = 0; q < 2 * R; ++q) tot[q] = CT(0);
-    for (int q = 0; q < ncw; ++q) {
-      const CT* src = rd + q * 2 * R;
-#pragma unroll
-      for (int u = 0; u < 2 * R; ++u) tot[u] += src[u];
+    for (int u = 0; u < R; ++u) {
+      tot[2 * u] = tot2[u].x;
+      tot[2 * u + 1] = tot2[u].y;
     }
 
     // phase 2: dx = rstd * (g - mean(g) - xhat * mean(g*xhat))

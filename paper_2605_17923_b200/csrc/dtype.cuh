@@ -259,6 +259,32 @@ __device__ __forceinline__ bool finite_ct(CT v) {
   return isfinite(v);
 }
 
+// Reduce NV per-lane values across the warp with a reduce-scatter butterfly: log2(NV) halving
+// exchanges, then plain butterflies.  Lanes [k * 32/NV, (k+1) * 32/NV) end with the complete
+// sum of value k (all of them bit-identical).  NV + 5 - log2(NV) shuffles instead of 5 * NV.
+template <int NV, typename CT>
+__device__ __forceinline__ CT warp_reduce_scatter(const CT* v, int lane) {
+  static_assert(NV == 1 || NV == 2 || NV == 4 || NV == 8, "NV must be 1, 2, 4 or 8");
+  CT w[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) w[i] = v[i];
+  int off = 16;
+#pragma unroll
+  for (int n = NV; n > 1; n >>= 1, off >>= 1) {
+    const bool hi = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const CT keep = hi ? w[i + n / 2] : w[i];
+      const CT send = hi ? w[i] : w[i + n / 2];
+      w[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  CT u = w[0];
+#pragma unroll
+  for (; off > 0; off >>= 1) u += __shfl_xor_sync(0xffffffffu, u, off);
+  return u;
+}
+
 template <typename CT>
 __device__ __forceinline__ CT warp_sum(CT v) {
 #pragma unroll
