@@ -177,26 +177,26 @@ const void* rows_kernel(int dtype, int vi, bool repack) {
   });
 }
 template <typename T>
-const void* rows_nopf(int vi) {
+const void* rows_pf(int vi) {
   switch (vi) {
-    case 0: return (const void*)al::adaln_fwd_rows<T, 1, true, false>;
-    case 1: return (const void*)al::adaln_fwd_rows<T, 2, true, false>;
-    case 2: return (const void*)al::adaln_fwd_rows<T, 3, true, false>;
-    case 3: return (const void*)al::adaln_fwd_rows<T, 4, true, false>;
-    case 4: return (const void*)al::adaln_fwd_rows<T, 6, true, false>;
-    case 5: return (const void*)al::adaln_fwd_rows<T, 8, true, false>;
-    case 6: return (const void*)al::adaln_fwd_rows<T, 12, true, false>;
-    case 7: return (const void*)al::adaln_fwd_rows<T, 16, true, false>;
-    case 8: return (const void*)al::adaln_fwd_rows<T, 20, true, false>;
-    default: return (const void*)al::adaln_fwd_rows<T, 24, true, false>;
+    case 0: return (const void*)al::adaln_fwd_rows<T, 1, true, true>;
+    case 1: return (const void*)al::adaln_fwd_rows<T, 2, true, true>;
+    case 2: return (const void*)al::adaln_fwd_rows<T, 3, true, true>;
+    case 3: return (const void*)al::adaln_fwd_rows<T, 4, true, true>;
+    case 4: return (const void*)al::adaln_fwd_rows<T, 6, true, true>;
+    case 5: return (const void*)al::adaln_fwd_rows<T, 8, true, true>;
+    case 6: return (const void*)al::adaln_fwd_rows<T, 12, true, true>;
+    case 7: return (const void*)al::adaln_fwd_rows<T, 16, true, true>;
+    case 8: return (const void*)al::adaln_fwd_rows<T, 20, true, true>;
+    default: return (const void*)al::adaln_fwd_rows<T, 24, true, true>;
   }
 }
-const void* rows_kernel_nopf(int dtype, int vi) {
+const void* rows_kernel_pf(int dtype, int vi) {
   switch (dtype) {
-    case AL_BF16: return rows_nopf<__nv_bfloat16>(vi);
-    case AL_F16: return rows_nopf<__half>(vi);
-    case AL_F64: return rows_nopf<double>(vi);
-    default: return rows_nopf<float>(vi);
+    case AL_BF16: return rows_pf<__nv_bfloat16>(vi);
+    case AL_F16: return rows_pf<__half>(vi);
+    case AL_F64: return rows_pf<double>(vi);
+    default: return rows_pf<float>(vi);
   }
 }
 const void* generic_kernel(int kernel, int dtype) {
@@ -323,11 +323,11 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
       pl.threads = 256;
       pl.smem = 2 * static_cast<size_t>(D) * cs;
       // variant 1 = keep packed (re-expand per pass), 2 = compiler's choice; default by width
-      // variant: 0 auto (packed + L2 prefetch), 1 packed, 2 compiler-expanded, 3 packed without
-      // the L2 prefetch of the next row
+      // variant: 0 auto (= 1), 1 packed row, 2 compiler-expanded row, 3 packed row + bulk L2
+      // prefetch of each warp's next row (slower on B200: 4.95 vs 5.53 TB/s at cfg2)
       const bool repack = tu.variant != 2;
       pl.R = repack ? 1 : 0;
-      pl.fn = tu.variant == 3 ? rows_kernel_nopf(dtype, vi) : rows_kernel(dtype, vi, repack);
+      pl.fn = tu.variant == 3 ? rows_kernel_pf(dtype, vi) : rows_kernel(dtype, vi, repack);
     } else if (ring_plan(kernel, nvec, row_bytes, cs, tu, &pl)) {
       const bool full = kernel == 1 && nvec == static_cast<int64_t>(pl.V) * (pl.threads - 32);
       pl.fn = tma_kernel(kernel, dtype, pl.V, pl.R, full);

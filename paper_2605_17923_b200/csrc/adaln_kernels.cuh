@@ -121,7 +121,7 @@ struct StageWalker {
 // about half the registers -> twice the resident warps); false lets the compiler keep it
 // expanded.
 // =====================================================================================
-template <typename T, int VPL, bool PACKED, bool PREFETCH = true>
+template <typename T, int VPL, bool PACKED, bool PREFETCH = false>
 __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
     __syncthreads();
     for (int64_t row = row0 + warp; row < seg_end; row += nwarp) {
       const uint8_t* xr = static_cast<const uint8_t*>(p.x) + row * RB;
-      // warm L2 with this warp's next row while this one is loaded and computed
+      // optional: warm L2 with this warp's next row (measured slower on B200: off by default)
       if (PREFETCH && lane == 0 && row + nwarp < seg_end) prefetch_l2_bulk(xr + nwarp * RB, RB);
       uint4 v[VPL];
 #pragma unroll
