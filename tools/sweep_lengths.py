@@ -1,0 +1,75 @@
+#!/usr/bin/env python3
+"""BASELINE configs[0] and [2]: cfg1 (fp32 fwd, B=2, S=1024, D=1536) and the mixed-length bf16
+fwd+bwd sweep at D=5120, S = 1560 ... 75600 (Wan-2.1 lambda=4 shapes).  One JSON line per
+config: achieved GB/s of algorithmic bytes and fraction of measured HBM peak.
+
+Small configs fit in L2 (126 MB), so each timed iteration rotates through enough input copies to
+exceed L2 (stated in the output as `l2`).
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+from bench import adaln_bytes, peak_hbm  # noqa: E402
+from paper_2605_17923_b200.adaln._ops import fused_backward, fused_forward  # noqa: E402
+
+L2_BYTES = 126 << 20
+
+
+def run(b, s, d, dtype, fwd_only, iters=20):
+    dev = torch.device("cuda", 0)
+    es = torch.tensor([], dtype=dtype).element_size()
+    per = b * s * d * es * (1 if fwd_only else 2)
+    copies = max(1, -(-3 * L2_BYTES // per)) if per < 3 * L2_BYTES else 1
+    sets = []
+    for _ in range(copies):
+        x = torch.randn(b, s, d, device=dev).to(dtype)
+        sc = (0.1 * torch.randn(b, d, device=dev)).to(dtype)
+        sh = (0.1 * torch.randn(b, d, device=dev)).to(dtype)
+        dy = None if fwd_only else torch.randn(b, s, d, device=dev).to(dtype)
+        sets.append((x, sc, sh, dy))
+
+    def step(i):
+        x, sc, sh, dy = sets[i % copies]
+        y, mu, rs = fused_forward(x, sc, sh)
+        if not fwd_only:
+            fused_backward(dy, x, sc, mu, rs)
+
+    for i in range(3):
+        step(i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(iters):
+        step(i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    nb = adaln_bytes(b * s, d, b, es)
+    nbytes = nb["fwd"] if fwd_only else nb["total"]
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    peak, kind = peak_hbm()
+    return {"B": b, "S": s, "D": d, "dtype": str(dtype).split(".")[-1],
+            "pass": "fwd" if fwd_only else "fwd+bwd", "ms": round(ms, 5),
+            "bytes": nbytes, "gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak, 4),
+            "l2": f"rotating {copies} input set(s)" if copies > 1 else "inputs larger than L2"}
+
+
+def main():
+    print(json.dumps({"config": "cfg1", **run(2, 1024, 1536, torch.float32, True, iters=50)}),
+          flush=True)
+    for s in (1560, 3600, 7800, 14040, 20280, 32760, 46800, 61200, 75600):
+        print(json.dumps({"config": "cfg3", **run(1, s, 5120, torch.bfloat16, False)}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
