@@ -4,7 +4,8 @@ fwd+bwd sweep at D=5120, S = 1560 ... 75600 (Wan-2.1 lambda=4 shapes).  One JSON
 config: achieved GB/s of algorithmic bytes and fraction of measured HBM peak.
 
 Small configs fit in L2 (126 MB), so each timed iteration rotates through enough input copies to
-exceed L2 (stated in the output as `l2`).
+exceed L2 (stated in the output as `l2`).  The timed iterations are replayed from one CUDA graph
+(host launch cost excluded: cfg1's kernel is ~5 us, shorter than the Python call path).
 """
 
 from __future__ import annotations
@@ -46,10 +47,20 @@ def run(b, s, d, dtype, fwd_only, iters=20):
     for i in range(3):
         step(i)
     torch.cuda.synchronize()
+    # capture `iters` steps in one CUDA graph so small configs are not bound by host launch cost
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g):
+            for i in range(iters):
+                step(i)
+    torch.cuda.current_stream().wait_stream(side)
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for i in range(iters):
-        step(i)
+    g.replay()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters
