@@ -269,7 +269,16 @@ def run_policy_steps(runner: DPStepRunner, sampler: BucketSampler, steps: int,
 def summarize(stats: list, world: int) -> dict:
     tok = sum(s.tokens for s in stats)
     t = sum(s.t_step_ms for s in stats) / 1e3
+    per_bucket = {}
+    for st in stats:
+        for sh, ti in zip(st.shards, st.t_compute_ms):
+            per_bucket.setdefault(f"{sh.batch_size}x{sh.seq_len}", []).append(ti)
     return {
+        "measured_ms_by_bucket": {k: round(float(np.mean(v)), 3) for k, v in
+                                  sorted(per_bucket.items(), key=lambda kv: int(kv[0].split("x")[1]))},
+        "per_step": [{"seq": [sh.seq_len for sh in st.shards],
+                      "t_ms": [round(x, 2) for x in st.t_compute_ms],
+                      "step_ms": round(st.t_step_ms, 2)} for st in stats],
         "steps": len(stats),
         "tokens_per_sec": tok / t if t > 0 else 0.0,
         "mean_step_ms": 1e3 * t / max(len(stats), 1),
