@@ -255,6 +255,23 @@ def plan_from_fit(kind: str, model, catalog, m_mem: float):
     return time_balanced_plan(model, catalog, m_mem)
 
 
+def warm_buckets(runner: DPStepRunner, plan) -> None:
+    """Run every planned (B, S) shape once on this rank (no collective) so kernels, workspaces
+    and the caching allocator's blocks exist before timing; without it a rank's first encounter
+    of a shape costs ~2x (allocator growth), which reads as imbalance."""
+    for e in plan.entries:
+        shard = RankShard(runner.rank, -1, e.bucket, e.batch_size)
+        x, t, target = runner.make_batch(shard)
+        with torch.autocast(runner.device.type, dtype=torch.bfloat16,
+                            enabled=runner.device.type == "cuda"):
+            loss = F.mse_loss(runner.block(x, t).float(), target.float())
+        loss.backward()
+        runner.flat_grad.zero_()
+        del x, t, target, loss
+    if runner.device.type == "cuda":
+        torch.cuda.synchronize(runner.device)
+
+
 def run_policy_steps(runner: DPStepRunner, sampler: BucketSampler, steps: int,
                      warmup: int = 0) -> list:
     stats = []
@@ -350,6 +367,7 @@ def bench_main(args, rest, world: int, rank: int, local: int) -> None:
         torch.manual_seed(0)
         runner = DPStepRunner(WanStyleBlock(), dev, world, rank, seed=extra.seed)
         sampler = BucketSampler(catalog, weights, plan, max(world, 1), extra.seed)
+        warm_buckets(runner, plan)
         stats = run_policy_steps(runner, sampler, steps, warmup=args.warmup)
         out[name] = summarize(stats, world)
         del runner
