@@ -323,6 +323,27 @@ def run_ours(args, world, rank, local):
     d2h = (x.numel() * es + 2 * S * 4) + (x.numel() * es + 2 * D * 4)
     e2e_gbs = world * nb["total"] / e2e_s / 1e9
 
+    # measured 'N-GPU imbalance %' of the metric: the DP step A/B (equal-token vs the
+    # B200-calibrated dual constraint) on this process group, N > 1 only
+    dp = None
+    if world > 1 and not args.no_dp:
+        del x, dy, xh, dyh, out, gr
+        torch.cuda.empty_cache()
+        try:
+            from paper_2605_17923_b200 import dp_step
+
+            r = dp_step.run_ab(world, rank, local, steps=args.dp_steps, warmup=2, detail=False)
+            pol = r["policies"]
+            dp = {"workload": r["config"]["workload"], "steps_per_policy": args.dp_steps,
+                  "plan_equal_token": r["config"]["plan_equal_token"],
+                  "plan_dual": r["config"]["plan_dual"], **r["imbalance"],
+                  "tokens_per_sec_equal_token": pol["equal_token"]["tokens_per_sec"],
+                  "tokens_per_sec_dual": pol["dual"]["tokens_per_sec"],
+                  "throughput_gain_vs_equal_token": r["throughput_gain_vs_equal_token"],
+                  "measured_ms_by_bucket_dual": pol["dual"]["measured_ms_by_bucket"],
+                  "predicted_ms_dual": (r["calibration"] or {}).get("predicted_ms")}
+        except Exception as exc:  # noqa: BLE001 - the kernel line must still be printed
+            dp = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if rank != 0:
         return
     # CPU baseline: the reference algorithm, single thread (as the numba reference runs)
@@ -370,6 +391,8 @@ def run_ours(args, world, rank, local):
         "clocks": clk.summary(),
         "imbalance": imbalance_summary(world),
     }
+    if dp is not None:
+        line["dp_step"] = dp
     print(json.dumps(line), flush=True)
 
 
@@ -387,6 +410,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-dp", action="store_true", help="skip the N>1 DP-step imbalance A/B")
+    ap.add_argument("--dp-steps", type=int, default=16)
     args, rest = ap.parse_known_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup(args)

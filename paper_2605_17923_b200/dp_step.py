@@ -306,42 +306,31 @@ def summarize(stats: list, world: int) -> dict:
 
 
 # ------------------------------------------------------------------------------ bench entry
-def bench_main(args, rest, world: int, rank: int, local: int) -> None:
-    """``bench.py --workload dit``: tokens/s of the balanced step at N GPUs (dual-constraint
-    plan) next to the equal-token baseline, with measured and load imbalance."""
-    import argparse
-
+def run_ab(world: int, rank: int, local: int, steps: int, warmup: int, seed: int = 42,
+           token_budget: int = 480_000, m_comp: float = 0.0, plan_kind: str = "calibrated",
+           cost_model: str = "quadratic", detail: bool = True) -> dict:
+    """Equal-token vs dual-constraint A/B of the DP step on this process group.  Returns the
+    result dict on every rank (rank 0's calibration is broadcast so plans agree)."""
     from .catalogs import reference_default_catalog
+    from .scheduler import DualConstraint, TokenBudget
 
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--policy-steps", type=int, default=0)
-    ap.add_argument("--seed", type=int, default=42)
-    ap.add_argument("--token-budget", type=int, default=480_000)
-    ap.add_argument("--m-comp", type=float, default=0.0)
-    ap.add_argument("--plan", choices=["calibrated", "reference"], default="calibrated")
-    ap.add_argument("--cost-model", choices=["quadratic", "power"], default="quadratic")
-    extra = ap.parse_args(rest)
     dev = torch.device("cuda", local)
     catalog, weights, tb, dc = reference_default_catalog()
     # the reference's defaults (480k-token envelope, M_comp = 3e9, p = 2: cluster_sim.py:328-336);
-    # a different --token-budget scales M_comp to keep the reference's M_comp / M_mem^2
-    m_mem = extra.token_budget
-    m_comp = extra.m_comp or dc.m_comp * (m_mem / dc.m_mem) ** 2
-    from .scheduler import DualConstraint, TokenBudget
-
+    # a different token budget scales M_comp to keep the reference's M_comp / M_mem^2
+    m_mem = token_budget
+    m_comp = m_comp or dc.m_comp * (m_mem / dc.m_mem) ** 2
     plan_a = emit_plan(catalog, TokenBudget(m_mem))
     plan_b = emit_plan(catalog, DualConstraint(float(m_mem), m_comp, 2.0))
     calib = None
-    if extra.plan == "calibrated":
-        # rank 0 measures and fits; the fit is broadcast so every rank plans identically (the
-        # plan must be common for the draws to stay rank-consistent)
+    if plan_kind == "calibrated":
         from .costfit import CostModel, QuadraticCostModel
 
         vec = torch.zeros(8, dtype=torch.float64, device=dev)
         trials = []
         if rank == 0:
             torch.manual_seed(0)
-            cal_runner = DPStepRunner(WanStyleBlock(), dev, 1, 0, seed=extra.seed)
+            cal_runner = DPStepRunner(WanStyleBlock(), dev, 1, 0, seed=seed)
             fits, trials = calibrate_plan(cal_runner, catalog, m_mem)
             pw, qd = fits["power"], fits["quadratic"]
             vec = torch.tensor([pw.a, pw.b, pw.p, pw.r2, qd.a, qd.c1, qd.c2, qd.r2],
@@ -354,47 +343,71 @@ def bench_main(args, rest, world: int, rank: int, local: int) -> None:
             dist.broadcast(vec, 0)
         v = [float(a) for a in vec.cpu()]
         fits = {"power": CostModel(*v[:4]), "quadratic": QuadraticCostModel(*v[4:])}
-        plan_b = plan_from_fit(extra.cost_model, fits[extra.cost_model], catalog, m_mem)
-        calib = {"cost_model": extra.cost_model,
+        plan_b = plan_from_fit(cost_model, fits[cost_model], catalog, m_mem)
+        calib = {"cost_model": cost_model,
                  "power_fit": fits["power"].__dict__, "quadratic_fit": fits["quadratic"].__dict__,
                  "trials": [[t.batch, t.seq_len, round(t.step_time, 6)] for t in trials],
-                 "predicted_ms": [round(1e3 * fits[extra.cost_model].predict(e.batch_size,
-                                                                             e.bucket.seq_len), 3)
+                 "predicted_ms": [round(1e3 * fits[cost_model].predict(e.batch_size,
+                                                                       e.bucket.seq_len), 3)
                                   for e in plan_b.entries]}
-    steps = extra.policy_steps or args.steps
     out = {}
     for name, plan in (("equal_token", plan_a), ("dual", plan_b)):
         torch.manual_seed(0)
-        runner = DPStepRunner(WanStyleBlock(), dev, world, rank, seed=extra.seed)
-        sampler = BucketSampler(catalog, weights, plan, max(world, 1), extra.seed)
+        runner = DPStepRunner(WanStyleBlock(), dev, world, rank, seed=seed)
+        sampler = BucketSampler(catalog, weights, plan, max(world, 1), seed)
         warm_buckets(runner, plan)
-        stats = run_policy_steps(runner, sampler, steps, warmup=args.warmup)
+        stats = run_policy_steps(runner, sampler, steps, warmup=warmup)
         out[name] = summarize(stats, world)
+        if not detail:
+            out[name].pop("per_step", None)
         del runner
         torch.cuda.empty_cache()
+    return {
+        "config": {"workload": "Wan-2.1-1.3B-style block (D=1536, 12 heads, FFN 8960), fused "
+                               "AdaLN x2, reference default catalog, per-rank draws",
+                   "token_budget": m_mem, "plan": plan_kind,
+                   "plan_equal_token": plan_a.batch_sizes(), "plan_dual": plan_b.batch_sizes(),
+                   "parallelism": f"dp{world}, one NCCL all-reduce per step", "steps": steps},
+        "policies": out,
+        "calibration": calib,
+        "imbalance": {
+            "compute_cv_equal_token_pct": out["equal_token"]["mean_compute_cv"],
+            "compute_cv_dual_pct": out["dual"]["mean_compute_cv"],
+            "cv_step_measured_equal_token": out["equal_token"]["mean_cv_step_measured"],
+            "cv_step_measured_dual": out["dual"]["mean_cv_step_measured"],
+            "wait_sync_ms_equal_token": out["equal_token"]["mean_wait_sync_ms"],
+            "wait_sync_ms_dual": out["dual"]["mean_wait_sync_ms"],
+        },
+        "throughput_gain_vs_equal_token": (out["dual"]["tokens_per_sec"]
+                                           / max(out["equal_token"]["tokens_per_sec"], 1e-9)
+                                           - 1.0),
+    }
+
+
+def bench_main(args, rest, world: int, rank: int, local: int) -> None:
+    """``bench.py --workload dit``: tokens/s of the balanced step at N GPUs (dual-constraint
+    plan) next to the equal-token baseline, with measured and load imbalance."""
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--policy-steps", type=int, default=0)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--token-budget", type=int, default=480_000)
+    ap.add_argument("--m-comp", type=float, default=0.0)
+    ap.add_argument("--plan", choices=["calibrated", "reference"], default="calibrated")
+    ap.add_argument("--cost-model", choices=["quadratic", "power"], default="quadratic")
+    extra = ap.parse_args(rest)
+    steps = extra.policy_steps or args.steps
+    res = run_ab(world, rank, local, steps, args.warmup, extra.seed, extra.token_budget,
+                 extra.m_comp, extra.plan, extra.cost_model)
     if rank == 0:
+        dual = res["policies"]["dual"]
         line = {
             "metric": "DiT-block DP step tokens/s (dual-constraint buckets)",
-            "value": round(out["dual"]["tokens_per_sec"], 1), "unit": "tokens/s",
+            "value": round(dual["tokens_per_sec"], 1), "unit": "tokens/s",
             "n_gpus": world, "steps": steps, "warmup": args.warmup,
-            "ms_per_step": round(out["dual"]["mean_step_ms"], 3), "higher_is_better": True,
+            "ms_per_step": round(dual["mean_step_ms"], 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "Wan-2.1-1.3B-style block (D=1536, 12 heads, FFN 8960), fused "
-                                   "AdaLN x2, reference default catalog, per-rank draws",
-                       "token_budget": m_mem, "plan": extra.plan,
-                       "plan_equal_token": plan_a.batch_sizes(),
-                       "plan_dual": plan_b.batch_sizes(),
-                       "parallelism": f"dp{world}, one NCCL all-reduce per step"},
-            "policies": out,
-            "calibration": calib,
-            "imbalance": {
-                "compute_cv_equal_token_pct": out["equal_token"]["mean_compute_cv"],
-                "compute_cv_dual_pct": out["dual"]["mean_compute_cv"],
-                "cv_step_measured_equal_token": out["equal_token"]["mean_cv_step_measured"],
-                "cv_step_measured_dual": out["dual"]["mean_cv_step_measured"],
-            },
-            "throughput_gain_vs_equal_token": (out["dual"]["tokens_per_sec"]
-                                               / max(out["equal_token"]["tokens_per_sec"], 1e-9)
-                                               - 1.0),
+            **res,
         }
         print(json.dumps(line), flush=True)
