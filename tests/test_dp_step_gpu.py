@@ -1,0 +1,67 @@
+"""DP step on one B200: the Wan-style block through the fused AdaLN autograd node, the flat
+gradient buffer, and the calibration sweep/fit (short)."""
+
+import pytest
+import torch
+
+from paper_2605_17923_b200.catalogs import reference_default_catalog
+from paper_2605_17923_b200.costfit import fit_quadratic_cost_model, time_balanced_plan
+from paper_2605_17923_b200.dp_step import (
+    BlockConfig, DPStepRunner, WanStyleBlock, measure_trials, run_policy_steps, summarize,
+    warm_buckets)
+from paper_2605_17923_b200.sampler import BucketSampler
+from paper_2605_17923_b200.scheduler import TokenBudget, emit_plan
+
+pytestmark = pytest.mark.gpu
+
+
+def torch_adaln(x, scale, shift, eps):
+    xf = x.float()
+    mu = xf.mean(-1, keepdim=True)
+    var = xf.var(-1, unbiased=False, keepdim=True)
+    y = (xf - mu) / torch.sqrt(var + eps) * (1 + scale.float()[:, None]) + shift.float()[:, None]
+    return y.to(x.dtype)
+
+
+def test_block_gradients_match_torch_adaln(cuda):
+    """Same block, fused sm_100a AdaLN vs a torch LayerNorm-Modulate: grads agree (bf16)."""
+    cfg = BlockConfig(dim=256, heads=4, ffn=512)
+    torch.manual_seed(0)
+    a = WanStyleBlock(cfg).to(cuda)
+    torch.manual_seed(0)
+    b = WanStyleBlock(cfg, norm_fn=torch_adaln).to(cuda)
+    g = torch.Generator(device=cuda).manual_seed(1)
+    x = torch.randn(2, 64, 256, device=cuda, generator=g, dtype=torch.bfloat16)
+    t = torch.randn(2, 256, device=cuda, generator=g, dtype=torch.bfloat16)
+    for m in (a, b):
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            m(x, t).float().square().mean().backward()
+    for (n, pa), (_, pb) in zip(a.named_parameters(), b.named_parameters()):
+        rel = (pa.grad - pb.grad).abs().max() / pb.grad.abs().max().clamp_min(1e-12)
+        assert rel.item() < 5e-2, n
+
+
+def test_dp_runner_single_gpu_steps(cuda):
+    cat, w, tb, dc = reference_default_catalog()
+    small = [b for b in cat if b.seq_len <= 9600]
+    ws = [b.sample_count for b in small]
+    ws = [v / sum(ws) for v in ws]
+    plan = emit_plan(small, TokenBudget(20_000))
+    runner = DPStepRunner(WanStyleBlock(BlockConfig(dim=256, heads=4, ffn=512)), cuda, 1, 0)
+    warm_buckets(runner, plan)
+    stats = run_policy_steps(runner, BucketSampler(small, ws, plan, 1, 0), 3, warmup=1)
+    s = summarize(stats, 1)
+    assert s["steps"] == 3 and s["tokens_per_sec"] > 0
+    assert all(p.grad.untyped_storage().data_ptr() == runner.flat_grad.untyped_storage().data_ptr()
+               for p in runner.params)
+
+
+def test_calibration_fit_is_tight(cuda):
+    runner = DPStepRunner(WanStyleBlock(BlockConfig(dim=256, heads=4, ffn=512)), cuda, 1, 0)
+    reqs = [(b, s) for s in (512, 1024, 2048, 4096) for b in (1, 2, 4)]
+    trials = measure_trials(runner, reqs, reps=2)
+    q = fit_quadratic_cost_model(trials)
+    assert q.r2 > 0.95
+    cat, *_ = reference_default_catalog()
+    plan = time_balanced_plan(q, cat, 480_000)
+    assert plan.entries[-1].batch_size >= 1
