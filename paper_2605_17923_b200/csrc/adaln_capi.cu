@@ -199,6 +199,24 @@ const void* rows_kernel_pf(int dtype, int vi) {
     default: return rows_pf<float>(vi);
   }
 }
+template <typename T>
+const void* rows16(int vi) {
+  switch (vi) {
+    case 0: return (const void*)al::adaln_fwd_rows16<T, 1>;
+    case 1: return (const void*)al::adaln_fwd_rows16<T, 2>;
+    case 2: return (const void*)al::adaln_fwd_rows16<T, 3>;
+    case 3: return (const void*)al::adaln_fwd_rows16<T, 4>;
+    case 4: return (const void*)al::adaln_fwd_rows16<T, 6>;
+    case 5: return (const void*)al::adaln_fwd_rows16<T, 8>;
+    case 6: return (const void*)al::adaln_fwd_rows16<T, 12>;
+    case 7: return (const void*)al::adaln_fwd_rows16<T, 16>;
+    case 8: return (const void*)al::adaln_fwd_rows16<T, 20>;
+    default: return (const void*)al::adaln_fwd_rows16<T, 24>;
+  }
+}
+const void* rows16_kernel(int dtype, int vi) {
+  return dtype == AL_BF16 ? rows16<__nv_bfloat16>(vi) : rows16<__half>(vi);
+}
 const void* generic_kernel(int kernel, int dtype) {
   return with_table(dtype, [&](const auto& t) {
     return kernel ? (const void*)t.bwd_generic : (const void*)t.fwd_generic;
@@ -323,11 +341,15 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
       pl.threads = 256;
       pl.smem = 2 * static_cast<size_t>(D) * cs;
       // variant 1 = keep packed (re-expand per pass), 2 = compiler's choice; default by width
-      // variant: 0 auto (= 1), 1 packed row, 2 compiler-expanded row, 3 packed row + bulk L2
-      // prefetch of each warp's next row (slower on B200: 4.95 vs 5.53 TB/s at cfg2)
+      // variant: 0 auto (16-bit rows -> mixed-precision single-pass kernel, else 1),
+      // 1 packed row, 2 compiler-expanded row, 3 packed row + bulk L2 prefetch of each warp's
+      // next row (slower on B200: 4.95 vs 5.53 TB/s at cfg2), 4 mixed-precision 16-bit kernel
+      const bool is16 = dtype == AL_BF16 || dtype == AL_F16;
+      const bool mixed = is16 && (tu.variant == 0 || tu.variant == 4);
       const bool repack = tu.variant != 2;
-      pl.R = repack ? 1 : 0;
-      pl.fn = tu.variant == 3 ? rows_kernel_pf(dtype, vi) : rows_kernel(dtype, vi, repack);
+      pl.R = mixed ? 2 : (repack ? 1 : 0);
+      pl.fn = mixed ? rows16_kernel(dtype, vi)
+                    : (tu.variant == 3 ? rows_kernel_pf(dtype, vi) : rows_kernel(dtype, vi, repack));
     } else if (ring_plan(kernel, nvec, row_bytes, cs, tu, &pl)) {
       const bool full = kernel == 1 && nvec == static_cast<int64_t>(pl.V) * (pl.threads - 32);
       pl.fn = tma_kernel(kernel, dtype, pl.V, pl.R, full);
@@ -419,6 +441,12 @@ int al_device_init(int device) {
           if (rc) return rc;
           rc = ensure_attr(rows_kernel(dt, vi, true), device);
           if (rc) return rc;
+          rc = ensure_attr(rows_kernel_pf(dt, vi), device);
+          if (rc) return rc;
+          if (dt == AL_BF16 || dt == AL_F16) {
+            rc = ensure_attr(rows16_kernel(dt, vi), device);
+            if (rc) return rc;
+          }
         }
       cudaFuncAttributes fa;
       e = cudaFuncGetAttributes(&fa, generic_kernel(kernel, dt));

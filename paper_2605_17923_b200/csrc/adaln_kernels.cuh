@@ -259,6 +259,111 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
 }
 
 // =====================================================================================
+// Forward, row-in-registers path for 16-bit rows (bf16 / fp16): the row stays packed in
+// registers and is consumed by mixed-precision subtracts (FHADD.{BF16,F16}: 16-bit operand,
+// fp32 result), so there is no separate expansion step.  Statistics in one pass over the
+// shifted values d = x - K (K = the row's first element): mean = K + sum(d)/D and
+// M2 = sum(d^2) - sum(d)^2/D -- the shift keeps the cancellation at the level of
+// (K - mean)^2 / var, far below the 16-bit inputs' own rounding.  Second pass writes
+// y = (x - mean) * rstd * (1 + scale) + shift.  About 5 instructions per element instead of 8.
+// =====================================================================================
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256) adaln_fwd_rows16(const FwdParams p) {
+  static_assert(sizeof(T) == 2, "16-bit rows only");
+  using P = float2;
+  constexpr int NP = 4;  // pairs per 16-byte vector
+  extern __shared__ __align__(16) uint8_t smem[];
+  P* s1 = reinterpret_cast<P*>(smem);  // [nvec * NP] : 1 + scale
+  P* sh = s1 + p.nvec * NP;            // [nvec * NP] : shift
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+  const float invD = 1.0f / static_cast<float>(p.D);
+  const float eps = static_cast<float>(p.eps);
+  const int RB = p.row_bytes;
+  bool nf = false;
+
+  int64_t row0 = r0;
+  while (row0 < r1) {
+    const int64_t g = row0 / p.S_grp;
+    const int64_t seg_end = min(r1, (g + 1) * p.S_grp);
+    __syncthreads();  // every warp is done with the previous group's modulation
+    {
+      const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
+      const uint8_t* sf = static_cast<const uint8_t*>(p.shift) + g * p.mod_stride * sizeof(T);
+      for (int c = tid; c < p.nvec; c += blockDim.x) {
+        P a[NP], b[NP];
+        unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sc) + c), a);
+        unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sf) + c), b);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y) && finite_ct(b[e].x) && finite_ct(b[e].y));
+          s1[c * NP + e] = add2(a[e], splat2(1.0f));
+          sh[c * NP + e] = b[e];
+        }
+      }
+    }
+    __syncthreads();
+    for (int64_t row = row0 + warp; row < seg_end; row += nwarp) {
+      const uint8_t* xr = static_cast<const uint8_t*>(p.x) + row * RB;
+      uint4 v[VPL];
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        v[i] = c < p.nvec ? ld_global_nc_v4(xr + c * 16) : make_uint4(0, 0, 0, 0);
+      }
+      P k0[NP];
+      unpack2<T>(v[0], k0);
+      const float K = __shfl_sync(0xffffffffu, k0[0].x, 0);
+      // pass 1: sum(d), sum(d^2) over valid vectors
+      P s[2] = {splat2(0.0f), splat2(0.0f)}, q[2] = {splat2(0.0f), splat2(0.0f)};
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        if (lane + 32 * i < p.nvec) {
+          const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const P dd = sub16x2_f32<T>(w[e], -K);
+            s[e & 1] = add2(s[e & 1], dd);
+            q[e & 1] = fma2(dd, dd, q[e & 1]);
+          }
+        }
+      }
+      const P ts = add2(s[0], s[1]), tq = add2(q[0], q[1]);
+      const float sd = warp_sum(ts.x + ts.y);
+      const float sq = warp_sum(tq.x + tq.y);
+      const float md = sd * invD;
+      const float m2 = fmaxf(sq - sd * md, 0.0f);
+      const float mean = K + md;
+      const float rs = 1.0f / sqrtf(m2 * invD + eps);
+      const P rs2 = splat2(rs);
+      // pass 2: y = (x - mean) * rstd * (1 + scale) + shift
+      uint8_t* yr = static_cast<uint8_t*>(p.y) + row * RB;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        if (c < p.nvec) {
+          const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+          P o[NP];
+#pragma unroll
+          for (int e = 0; e < NP; ++e)
+            o[e] = fma2(mul2(sub16x2_f32<T>(w[e], -mean), rs2), s1[c * NP + e], sh[c * NP + e]);
+          st_global_cs(yr + c * 16, pack2<T>(o));
+        }
+      }
+      if (lane == 0) {
+        static_cast<float*>(p.mean)[row] = mean;
+        static_cast<float*>(p.rstd)[row] = rs;
+        nf |= !(finite_ct(mean) && finite_ct(sq));
+      }
+    }
+    row0 = seg_end;
+  }
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+// =====================================================================================
 // Forward, wide-row TMA ring path (rows too wide for registers).
 // blockDim = nc consumers (multiple of 32) + 1 producer warp.  Stage = R rows streamed into
 // shared memory by 1-D bulk copies; consumer thread t owns 16-byte vectors t + i*nc.

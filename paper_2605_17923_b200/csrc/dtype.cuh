@@ -254,6 +254,25 @@ __device__ __forceinline__ uint4 ld_global_nc_v4(const void* p) {
   return v;
 }
 
+// ---- mixed-precision subtract: fp32 (x16 - k) straight from a packed 16-bit pair -------------
+// sm_100 `add.rn.f32.{bf16,f16}` (SASS FHADD) reads either half of a register directly, so the
+// 16-bit -> fp32 expansion costs nothing beyond the subtraction itself.
+template <typename T>
+__device__ __forceinline__ float2 sub16x2_f32(uint32_t w, float nk) {
+  static_assert(sizeof(T) == 2, "16-bit types only");
+  unsigned short lo, hi;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(w));
+  float a, b;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    asm("add.rn.f32.bf16 %0, %1, %2;" : "=f"(a) : "h"(lo), "f"(nk));
+    asm("add.rn.f32.bf16 %0, %1, %2;" : "=f"(b) : "h"(hi), "f"(nk));
+  } else {
+    asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(a) : "h"(lo), "f"(nk));
+    asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(b) : "h"(hi), "f"(nk));
+  }
+  return make_float2(a, b);
+}
+
 template <typename CT>
 __device__ __forceinline__ bool finite_ct(CT v) {
   return isfinite(v);
