@@ -36,6 +36,7 @@ import torch
 import torch.nn as nn
 import torch.nn.functional as F
 
+from .errors import AdaptiveLoadError
 from .sampler import BucketSampler, RankShard, compute_cv, cv_step
 from .scheduler import emit_plan
 
@@ -272,14 +273,52 @@ def warm_buckets(runner: DPStepRunner, plan) -> None:
         torch.cuda.synchronize(runner.device)
 
 
+@dataclass(frozen=True)
+class RefitConfig:
+    """Closed-loop recalibration (reference: cluster_sim.py:187-195, 238-241): every `every`
+    steps, refit the cost model on ALL ranks' measured (B_i, S_i, T_i) so far and re-plan.
+    The per-rank times are all-gathered each step, so every rank fits the same data and
+    arrives at the same plan without any extra communication."""
+
+    every: int
+    m_mem: float
+    cost_model: str = "quadratic"
+
+
 def run_policy_steps(runner: DPStepRunner, sampler: BucketSampler, steps: int,
-                     warmup: int = 0) -> list:
-    stats = []
+                     warmup: int = 0, refit: RefitConfig | None = None,
+                     refit_log: list | None = None) -> list:
+    from .costfit import (GridSpec, calibrated_dual_constraint, fit_cost_model,
+                          fit_quadratic_cost_model, time_balanced_plan)
+    from .traces import trials_from_steps
+
+    stats, trials = [], []
     for i in range(warmup + steps):
         shards = sampler.step()
         st = runner.step(i, shards)
         if i >= warmup:
             stats.append(st)
+        if refit is not None:
+            trials.extend(trials_from_steps([st])[0])
+            if (i + 1) % refit.every == 0 and len({(t.batch, t.seq_len) for t in trials}) >= 3:
+                try:
+                    if refit.cost_model == "power":
+                        model = fit_cost_model(trials, GridSpec(1.0, 2.4, 0.05))
+                        plan = emit_plan(sampler.catalog,
+                                         calibrated_dual_constraint(model, sampler.catalog,
+                                                                    refit.m_mem))
+                    else:
+                        model = fit_quadratic_cost_model(trials)
+                        plan = time_balanced_plan(model, sampler.catalog, refit.m_mem)
+                except AdaptiveLoadError as exc:  # keep the current plan (same on every rank)
+                    if refit_log is not None:
+                        refit_log.append({"step": i, "error": type(exc).__name__})
+                    continue
+                sampler.set_plan(plan)
+                warm_buckets(runner, plan)
+                if refit_log is not None:
+                    refit_log.append({"step": i, "model": model.__dict__,
+                                      "plan": plan.batch_sizes()})
     return stats
 
 

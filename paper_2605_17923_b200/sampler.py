@@ -107,6 +107,10 @@ class BucketSampler:
         self.noise_sigma = noise_sigma
         self.last_noise = None
 
+    def set_plan(self, plan: BucketPlan) -> None:
+        """Swap the per-bucket batch sizes (closed-loop refit); the draw stream is unaffected."""
+        self.batches = _planned(plan, self.catalog)
+
     def step(self) -> list[RankShard]:
         idx = draw_indices(self.cdf, self.world_size, self.rng)
         if self.noise_draws:
@@ -151,11 +155,13 @@ class PolicyMetrics:
     mean_t_sync: float
     tokens_per_sec: float         # total tokens / total synchronized time
     steps: int
+    rows: tuple = ()              # per-step metrics (traces.METRICS_COLUMNS) when requested
 
 
 def simulate_policy(catalog, weights, plan: BucketPlan, world_size: int, steps: int,
                     rng: np.random.Generator, cost: CostParams = CostParams(),
-                    noise_sigma: float = 0.03) -> PolicyMetrics:
+                    noise_sigma: float = 0.03, geom: LatentGeometry | None = None,
+                    keep_rows: bool = False) -> PolicyMetrics:
     """The reference's run_policy metrics without refit (cluster_sim.py:198-246).
 
     Consumes the generator exactly like the reference (N uniforms for the draw, then N normals
@@ -163,7 +169,8 @@ def simulate_policy(catalog, weights, plan: BucketPlan, world_size: int, steps: 
     """
     sampler = BucketSampler(catalog, weights, plan, world_size, rng, noise_draws=world_size,
                             noise_sigma=noise_sigma)
-    ccv, ccr, cvs, tcv, tsync, toks = [], [], [], [], [], []
+    geom = geom or LatentGeometry()
+    ccv, ccr, cvs, tcv, tsync, toks, rows = [], [], [], [], [], [], []
     for _ in range(steps):
         shards = sampler.step()
         noise = np.maximum(NOISE_FLOOR, 1.0 + sampler.last_noise)
@@ -176,10 +183,14 @@ def simulate_policy(catalog, weights, plan: BucketPlan, world_size: int, steps: 
         tcv.append(compute_cv(times))
         tsync.append(max(times))
         toks.append(sum(sh.tokens for sh in shards))
+        if keep_rows:
+            units = sum(latent_units(sh, geom) for sh in shards)
+            rows.append({"t_sync": tsync[-1], "cv_step": cvs[-1], "compute_cv": ccv[-1],
+                         "tokens_per_sec": toks[-1] / tsync[-1], "theta": units / tsync[-1]})
     t = np.asarray(tsync)
     return PolicyMetrics(float(np.mean(ccv)), float(np.mean(ccr)), float(np.mean(cvs)),
                          float(np.mean(tcv)), float(t.mean()), float(np.sum(toks) / t.sum()),
-                         steps)
+                         steps, tuple(rows))
 
 
 def compare_policies(catalog, weights, plan_baseline: BucketPlan, plan_dual: BucketPlan,
@@ -191,8 +202,9 @@ def compare_policies(catalog, weights, plan_baseline: BucketPlan, plan_dual: Buc
                         np.random.default_rng(child_a), cost, noise_sigma)
     b = simulate_policy(catalog, weights, plan_dual, world_size, steps,
                         np.random.default_rng(child_b), cost, noise_sigma)
+    strip = lambda m: {k: v for k, v in m.__dict__.items() if k != "rows"}  # noqa: E731
     return {
-        "equal_token": a.__dict__, "dual": b.__dict__,
+        "equal_token": strip(a), "dual": strip(b),
         "compute_cv_reduction": (a.mean_compute_cv - b.mean_compute_cv) / a.mean_compute_cv,
         "tokens_per_sec_gain": b.tokens_per_sec / a.tokens_per_sec - 1.0,
     }

@@ -1,0 +1,94 @@
+"""Trace, plan, model and metrics files in the reference's schemas (reference: io.py:99-203).
+
+SURVEY 8(f) rank 3: the B200 DP step emits its per-rank measurements in the same text formats
+the reference CLI reads (`fit` consumes trial JSONL, `simulate`/`plan` consume plan and model
+JSON, metrics go to CSV), so the reference tooling can fit, plan and compare on real B200
+traces.  Deterministic text: sorted keys, 2-space JSON indent, `repr` floats in CSV.
+"""
+
+from __future__ import annotations
+
+import csv
+import json
+from pathlib import Path
+
+from .costfit import CostModel, Trial
+from .scheduler import Binding, BucketPlan, PlanEntry
+from .shapes import Bucket, MediaShape
+
+__all__ = ["save_trace", "load_trace", "save_plan", "load_plan", "save_model", "load_model",
+           "save_metrics_csv", "METRICS_COLUMNS", "trials_from_steps"]
+
+METRICS_COLUMNS = ["step", "policy", "t_sync", "cv_step", "compute_cv", "tokens_per_sec", "theta"]
+
+
+def _write_json(path, doc) -> None:
+    Path(path).write_text(json.dumps(doc, sort_keys=True, indent=2) + "\n")
+
+
+def save_trace(path, trials, workers=None) -> None:
+    """One JSON object per line: batch, seq_len, step_time_sync (s) [, worker] (io.py:158-165)."""
+    lines = []
+    for i, t in enumerate(trials):
+        row = {"batch": t.batch, "seq_len": t.seq_len, "step_time_sync": t.step_time}
+        if workers is not None:
+            row["worker"] = workers[i]
+        lines.append(json.dumps(row, sort_keys=True))
+    Path(path).write_text("".join(line + "\n" for line in lines))
+
+
+def load_trace(path) -> list:
+    out = []
+    for line in Path(path).read_text().splitlines():
+        if line.strip():
+            r = json.loads(line)
+            out.append(Trial(r["batch"], r["seq_len"], r["step_time_sync"]))
+    return out
+
+
+def save_plan(path, plan: BucketPlan, manifest: dict | None = None) -> None:
+    entries = [{"frames": e.bucket.shape.frames, "height": e.bucket.shape.height,
+                "width": e.bucket.shape.width, "seq_len": e.bucket.seq_len,
+                "sample_count": e.bucket.sample_count, "batch_size": e.batch_size,
+                "binding": None if e.binding is None else e.binding.value}
+               for e in plan.entries]
+    _write_json(path, {"entries": entries, "manifest": manifest or {}})
+
+
+def load_plan(path) -> BucketPlan:
+    doc = json.loads(Path(path).read_text())
+    return BucketPlan(tuple(
+        PlanEntry(Bucket(MediaShape(e["frames"], e["height"], e["width"]), e["seq_len"],
+                         e["sample_count"]), e["batch_size"],
+                  None if e["binding"] is None else Binding(e["binding"]))
+        for e in doc["entries"]))
+
+
+def save_model(path, model: CostModel, manifest: dict | None = None) -> None:
+    _write_json(path, {"a": model.a, "b": model.b, "p": model.p, "r2": model.r2,
+                       "manifest": manifest or {}})
+
+
+def load_model(path) -> CostModel:
+    doc = json.loads(Path(path).read_text())
+    return CostModel(doc["a"], doc["b"], doc["p"], doc["r2"])
+
+
+def save_metrics_csv(path, rows_by_policy: dict) -> None:
+    """rows_by_policy: policy -> list of dicts with the METRICS_COLUMNS fields (per step)."""
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(METRICS_COLUMNS)
+        for policy, rows in rows_by_policy.items():
+            for i, r in enumerate(rows):
+                w.writerow([i, policy] + [repr(float(r[c])) for c in METRICS_COLUMNS[2:]])
+
+
+def trials_from_steps(stats) -> tuple[list, list]:
+    """Per-rank (B_i, S_i, T_i) of measured DP steps as reference Trials (seconds) + worker ids."""
+    trials, workers = [], []
+    for st in stats:
+        for rank, (sh, t_ms) in enumerate(zip(st.shards, st.t_compute_ms)):
+            trials.append(Trial(sh.batch_size, sh.seq_len, t_ms / 1e3))
+            workers.append(rank)
+    return trials, workers

@@ -235,7 +235,31 @@ def make_costfit():
     return res
 
 
+def make_io():
+    """Reference-written plan / model / trace / metrics files (tests/golden/io/)."""
+    from adaptiveload import io as rio
+    from adaptiveload.cluster_sim import run_experiment
+    from adaptiveload.costfit import Trial, fit_cost_model
+    from adaptiveload.manifest import RunManifest
+
+    d = OUT / "io"
+    d.mkdir(exist_ok=True)
+    cat, w = default_catalog()
+    man = RunManifest(command="plan", inputs=["catalog.json"], outputs=["plan.json"], seed=42,
+                      config_digest="0" * 64)
+    rio.save_plan(d / "plan_dual.json", emit_plan(cat, default_dual_constraint()), man)
+    rio.save_plan(d / "plan_equal_token.json", emit_plan(cat, default_token_budget()), man)
+    trials = [Trial(b, s, 2.0 + 1e-9 * b * s ** 2) for b, s in ((1, 1600), (3, 24000), (1, 52800))]
+    rio.save_trace(d / "trace.jsonl", trials, workers=[0, 1, 0])
+    rio.save_model(d / "model.json", fit_cost_model(trials), man)
+    res = run_experiment(cat, w, emit_plan(cat, default_token_budget()),
+                         emit_plan(cat, default_dual_constraint()),
+                         ClusterConfig(num_workers=4, steps=5, seed=42))
+    rio.save_metrics_csv(d / "metrics.csv", {"equal_token": res.series_a, "dual": res.series_b})
+
+
 if __name__ == "__main__":
     make_adaln()
     make_sampler()
+    make_io()
     print("wrote", sorted(p.name for p in OUT.iterdir()))

@@ -66,7 +66,24 @@ def _worker(rank, world, port, outdir):
     grads_ptr_ok = all(
         p.grad.untyped_storage().data_ptr() == runner.flat_grad.untyped_storage().data_ptr()
         for p in runner.params)
-    torch.save({"grad": runner.flat_grad.clone(), "times": st.t_compute_ms,
+    # closed-loop refit: identical gathered traces -> identical plans on every rank
+    from paper_2605_17923_b200.dp_step import RefitConfig, run_policy_steps
+
+    small = [b for b in cat if b.seq_len <= 9600]
+    plan0 = emit_plan(small, dc)
+    ws = [1.0 / len(small)] * len(small)
+
+    sm2 = BucketSampler(small, ws, plan0, world, 7)
+    # shrink the work: scale buckets down to CPU size by a custom batch maker
+    runner2 = DPStepRunner(WanStyleBlock(CFG, norm_fn=cpu_adaln), torch.device("cpu"), world, rank,
+                           dtype=torch.float32)
+    runner2.make_batch = lambda sh: batch_for(RankShard(sh.rank, sh.bucket_index,
+                                                        type(sh.bucket)(sh.bucket.shape, 8 + sh.bucket_index, 1),
+                                                        1 + sh.bucket_index % 2), 5)
+    log = []
+    run_policy_steps(runner2, sm2, 4, warmup=0, refit=RefitConfig(every=2, m_mem=480_000),
+                     refit_log=log)
+    torch.save({"grad": runner.flat_grad.clone(), "times": st.t_compute_ms, "refit": log,
                 "cv_step": st.cv_step, "compute_cv": st.compute_cv, "tokens": st.tokens,
                 "draws": draws, "grads_ptr_ok": grads_ptr_ok, "wait": st.wait_sync_ms},
                os.path.join(outdir, f"rank{rank}.pt"))
@@ -114,3 +131,9 @@ def test_imbalance_metrics(gloo_results):
     assert r0["compute_cv"] == pytest.approx(100 * np.std(loads) / np.mean(loads))
     assert r0["tokens"] == 3 * 12 + 2 * 20
     assert min(r0["wait"]) == 0.0
+
+
+def test_closed_loop_refit_agrees_across_ranks(gloo_results):
+    a, b = gloo_results[0]["refit"], gloo_results[1]["refit"]
+    assert len(a) == 2 and a == b
+    assert all("plan" in e or "error" in e for e in a)
