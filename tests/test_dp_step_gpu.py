@@ -57,11 +57,13 @@ def test_dp_runner_single_gpu_steps(cuda):
 
 
 def test_calibration_fit_is_tight(cuda):
-    runner = DPStepRunner(WanStyleBlock(BlockConfig(dim=256, heads=4, ffn=512)), cuda, 1, 0)
-    reqs = [(b, s) for s in (512, 1024, 2048, 4096) for b in (1, 2, 4)]
+    """Wan-1.3B widths: measured fwd+bwd times are linear + quadratic in S (R^2 > 0.99)."""
+    runner = DPStepRunner(WanStyleBlock(), cuda, 1, 0)
+    reqs = [(b, s) for s in (2048, 4096, 8192, 16384) for b in (1, 2, 4)]
     trials = measure_trials(runner, reqs, reps=2)
     q = fit_quadratic_cost_model(trials)
-    assert q.r2 > 0.95
+    assert q.r2 > 0.99 and q.c1 > 0
     cat, *_ = reference_default_catalog()
     plan = time_balanced_plan(q, cat, 480_000)
     assert plan.entries[-1].batch_size >= 1
+    assert plan.batch_sizes() == sorted(plan.batch_sizes(), reverse=True)
