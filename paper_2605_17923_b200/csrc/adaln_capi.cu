@@ -386,6 +386,18 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
   return AL_OK;
 }
 
+// Every CTA of a cooperative grid must be co-resident: grid <= SMs x resident CTAs.
+bool cooperative_ok(const Plan& pl) {
+  int dev, sms, occ = 0, coop = 0;
+  if (current_device(&dev) || dev_sms(dev, &sms)) return false;
+  if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) != cudaSuccess || !coop)
+    return false;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pl.fn, pl.threads, pl.smem) !=
+      cudaSuccess)
+    return false;
+  return pl.grid <= occ * sms;
+}
+
 int check_common(int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride, int dtype) {
   if (elem_size(dtype) == 0) return fail(AL_ERR_DTYPE, "unsupported dtype code %d", dtype);
   if (batch < 0 || seq < 0) return fail(AL_ERR_SHAPE, "batch/seq must be >= 0");
@@ -529,7 +541,8 @@ int64_t al_adaln_backward_workspace_bytes(int64_t batch, int64_t seq, int64_t di
   if (make_plan(1, N, dim, mod_stride, dtype, n_tile, aligned, 1, &pa)) return -1;
   if (make_plan(1, N, dim, mod_stride, dtype, n_tile, aligned, 1, &pg, true)) return -1;
   const int64_t ngroups = mod_stride ? batch : 1;
-  return 2 * (std::max(pa.grid, pg.grid) + ngroups - 1) * dim * ct_size(dtype);
+  // + 16 bytes: the fused stage-2 grid-barrier counter
+  return 2 * (std::max(pa.grid, pg.grid) + ngroups - 1) * dim * ct_size(dtype) + 16;
 }
 
 int al_adaln_backward(const void* dy, const void* x, const void* scale, const void* mean,
@@ -586,12 +599,37 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   p.row_bytes = static_cast<int>(dim * elem_size(dtype));
   p.nstages = pl.NS;
   p.G = pl.grid;
-  void* args[] = {&p};
-  cudaError_t e = cudaLaunchKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st);
-  if (e != cudaSuccess) return cuda_fail(e, "backward stage-1 launch");
-  // stage 2: 16-byte vector form when every partial row is 16-byte aligned
+  p.counter = nullptr;
+  p.dscale = dscale;
+  p.dshift = dshift;
   const int cs = ct_size(dtype);
   const bool vec = (dim * cs) % 16 == 0 && aligned16(workspace);
+  // Fused stage 2: the TMA kernel reduces the partials itself behind a grid barrier, which
+  // needs a cooperative launch (all CTAs co-resident) and a zeroed counter at the workspace
+  // tail.  Otherwise stage 2 is a second kernel.
+  bool fuse = false;
+  {
+    Tuning tu;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      tu = g_tune[1];
+    }
+    fuse = pl.path == 1 && vec && tu.variant != 1 &&
+           workspace_bytes >= need + 16 && cooperative_ok(pl);
+  }
+  void* args[] = {&p};
+  cudaError_t e;
+  if (fuse) {
+    p.counter = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(workspace) + need);
+    e = cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), st);
+    if (e != cudaSuccess) return cuda_fail(e, "memset");
+    e = cudaLaunchCooperativeKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st);
+    if (e != cudaSuccess) return cuda_fail(e, "backward (fused) cooperative launch");
+    return AL_OK;
+  }
+  e = cudaLaunchKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st);
+  if (e != cudaSuccess) return cuda_fail(e, "backward stage-1 launch");
+  // stage 2: 16-byte vector form when every partial row is 16-byte aligned
   const void* rk = reduce_kernel(dtype, vec);
   int64_t G64 = pl.grid;
   void* rargs[] = {&workspace, &dscale, &dshift, &p.N, &p.S_grp, &p.D, &G64, &p.nslots};

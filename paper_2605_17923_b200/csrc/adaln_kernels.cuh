@@ -70,6 +70,11 @@ struct BwdParams {
   int row_bytes;
   int nstages;
   int G;
+  // fused stage 2 (cooperative launch): grid barrier counter (zeroed by the host) and outputs;
+  // nullptr counter = stage 2 runs as the separate adaln_bwd_reduce* kernel
+  unsigned int* counter;
+  void* dscale;
+  void* dshift;
 };
 
 // Row partition shared by stage 1 and stage 2.
@@ -569,6 +574,76 @@ __global__ void __launch_bounds__(512) adaln_fwd_wide(const FwdParams p) {
 }
 
 // =====================================================================================
+// Fused stage 2 (cooperative launch only: every CTA of the grid is co-resident).
+// After its stage-1 partials are stored, each CTA passes a grid barrier (one atomic per CTA
+// on a host-zeroed counter), then reduces a contiguous share of the (group, 16-byte column
+// vector) items over the CTAs that cover the group: one warp per item, each lane summing a
+// strided subset of the slots in fp64, combined by a fixed butterfly -- deterministic, and
+// the same fp64 sum order for every call with the same launch geometry.
+// =====================================================================================
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename CT>
+__device__ void fused_stage2(const BwdParams& p, int nc, int tid) {
+  constexpr int VE = 16 / sizeof(CT);
+  const int lane = tid & 31, warp = tid >> 5, ncw = nc >> 5;
+  __threadfence();
+  named_bar_sync(1, nc);
+  if (tid == 0) {
+    atomicAdd(p.counter, 1u);
+    while (ld_acquire_gpu(p.counter) < static_cast<unsigned int>(p.G)) __nanosleep(64);
+  }
+  named_bar_sync(1, nc);
+  const int64_t nvecs = p.D / VE;
+  const int64_t ngroups = (p.N + p.S_grp - 1) / p.S_grp;
+  const int64_t items = ngroups * nvecs;
+  const int64_t per = (items + p.G - 1) / p.G;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * per;
+  const int64_t i1 = min(items, i0 + per);
+  const CT* ws = static_cast<const CT*>(p.ws);
+  for (int64_t it = i0 + warp; it < i1; it += ncw) {
+    const int64_t g = it / nvecs, cv = it % nvecs;
+    const int64_t first_row = g * p.S_grp;
+    const int64_t last_row = min((g + 1) * p.S_grp, p.N) - 1;
+    const int64_t kf = part_owner(first_row, p.N, p.G), kl = part_owner(last_row, p.N, p.G);
+    const CT* sc = ws + (kf + g) * p.D + cv * VE;
+    const CT* sh = ws + (p.nslots + kf + g) * p.D + cv * VE;
+    double a[VE], b[VE];
+#pragma unroll
+    for (int e = 0; e < VE; ++e) a[e] = b[e] = 0.0;
+    for (int64_t s = lane; s <= kl - kf; s += 32) {
+      const uint4 va = __ldcg(reinterpret_cast<const uint4*>(sc + s * p.D));
+      const uint4 vb = __ldcg(reinterpret_cast<const uint4*>(sh + s * p.D));
+      const CT* pa = reinterpret_cast<const CT*>(&va);
+      const CT* pb = reinterpret_cast<const CT*>(&vb);
+#pragma unroll
+      for (int e = 0; e < VE; ++e) {
+        a[e] += static_cast<double>(pa[e]);
+        b[e] += static_cast<double>(pb[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      a[e] = warp_sum(a[e]);
+      b[e] = warp_sum(b[e]);
+    }
+    if (lane == 0) {
+      CT* ds = static_cast<CT*>(p.dscale) + g * p.D + cv * VE;
+      CT* dh = static_cast<CT*>(p.dshift) + g * p.D + cv * VE;
+#pragma unroll
+      for (int e = 0; e < VE; ++e) {
+        ds[e] = static_cast<CT>(a[e]);
+        dh[e] = static_cast<CT>(b[e]);
+      }
+    }
+  }
+}
+
+// =====================================================================================
 // Backward stage 1, TMA ring path.  Stage layout: [x: R rows][dy: R rows].
 // Consumer thread t owns 16-byte column vectors t + i*nc (i < V): per row it forms
 // xhat = (x - mu) * rstd and g = dy * (1 + scale) once, keeps both in registers across the
@@ -818,6 +893,7 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
   }
   if (cur_g >= 0) flush(cur_g);
   if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+  if (p.counter != nullptr) fused_stage2<CT>(p, nc, tid);
 }
 
 // =====================================================================================

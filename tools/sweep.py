@@ -81,11 +81,12 @@ def main():
                 print(json.dumps({"kernel": "fwd", "cfg": c, "error": str(exc)[:200]}))
         nat.set_tuning(0)
     if "bwd" in args.which:
-        cfgs = [dict(V=V, R=R, smem=sm) for V, R, sm in itertools.product(
+        cfgs = [dict(V=0, R=0, smem=0, variant=v) for v in (0, 1)]  # fused vs separate stage 2
+        cfgs += [dict(V=V, R=R, smem=sm) for V, R, sm in itertools.product(
             (1, 2, 4), (1, 2, 4), (100 * 1024, 150 * 1024, 200 * 1024))]
         for c in cfgs:
             try:
-                nat.set_tuning(1, c["V"], c["R"], c["smem"], False, 0)
+                nat.set_tuning(1, c["V"], c["R"], c["smem"], False, c.get("variant", 0))
                 plan = nat.describe_launch(1, B, S, D, D, code)
                 ms = time_fn(lambda: fused_backward(dy, x, sc, mu, rs), args.iters)
                 report("bwd", c, ms, nb["bwd"], plan)
