@@ -92,8 +92,8 @@ AL_API int64_t al_adaln_backward_workspace_bytes(int64_t batch, int64_t seq, int
  * (_reduce_naive_kernel :71-83 / _dtile_kernel_* :94-127) in one pass over dy and x.
  * Stage 1: each CTA owns a contiguous row range and every thread owns fixed feature columns
  * (the paper's D-tile mapping); per-column fp32 partials go to `workspace`.  Stage 2 sums the
- * partials over CTAs in ascending CTA order (fp64 accumulator): in the same cooperative launch
- * behind a grid barrier when every CTA is co-resident, else as a second kernel.
+ * partials over CTAs in ascending CTA order (fp64 accumulator) in a second kernel (or, opt-in,
+ * in the same cooperative launch behind a grid barrier).
  * d_tile / n_tile: the reference TileConfig (adaln/__init__.py:70-73), validated with the
  * reference bounds (1 <= d_tile <= dim, 1 <= n_tile <= rows per reduction group); n_tile caps
  * the rows per stage-1 partial; 0/0 selects the default tiling (adaln_backward_naive).
@@ -111,8 +111,8 @@ AL_API int al_adaln_backward(const void* dy, const void* x, const void* scale,
  * vecs_per_thread in {1,2,4}; rows_per_stage in {1,2,4}; smem_budget in bytes per CTA;
  * force_generic = 1 routes through the generic (any-shape) kernels.  variant: forward -- the rows
  * kernel flavour (0 auto, 1 packed row, 2 compiler-expanded row, 3 packed + L2 prefetch,
- * 4 mixed-precision 16-bit); backward -- 0 fused stage 2 (cooperative launch, grid barrier),
- * 1 separate stage-2 kernel.  Process-global.  For the forward kernel a nonzero
+ * 4 mixed-precision 16-bit); backward -- 0 separate stage-2 kernel, 2 stage 2 fused into the
+ * stage-1 kernel behind a cooperative grid barrier.  Process-global.  For the forward kernel a nonzero
  * vecs_per_thread / rows_per_stage selects the wide (TMA ring) path.
  */
 AL_API int al_set_tuning(int kernel, int vecs_per_thread, int rows_per_stage, int smem_budget,

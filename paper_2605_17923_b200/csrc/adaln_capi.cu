@@ -614,7 +614,8 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
       std::lock_guard<std::mutex> lk(g_mu);
       tu = g_tune[1];
     }
-    fuse = pl.path == 1 && vec && tu.variant != 1 &&
+    // opt-in (variant 2): measured equal to the separate kernel on B200 (0.189 ms both)
+    fuse = pl.path == 1 && vec && tu.variant == 2 &&
            workspace_bytes >= need + 16 && cooperative_ok(pl);
   }
   void* args[] = {&p};

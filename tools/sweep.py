@@ -81,7 +81,7 @@ def main():
                 print(json.dumps({"kernel": "fwd", "cfg": c, "error": str(exc)[:200]}))
         nat.set_tuning(0)
     if "bwd" in args.which:
-        cfgs = [dict(V=0, R=0, smem=0, variant=v) for v in (0, 1)]  # fused vs separate stage 2
+        cfgs = [dict(V=0, R=0, smem=0, variant=v) for v in (0, 2)]  # separate vs fused stage 2
         cfgs += [dict(V=V, R=R, smem=sm) for V, R, sm in itertools.product(
             (1, 2, 4), (1, 2, 4), (100 * 1024, 150 * 1024, 200 * 1024))]
         for c in cfgs:
