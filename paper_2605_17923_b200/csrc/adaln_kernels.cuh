@@ -816,23 +816,12 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         const bool ok = live && (vmask >> j & 1);
-        P dv[NP];
-        const uint4 xr = ok ? ld_shared_v4(stx + rr * RB + coff[j]) : make_uint4(0, 0, 0, 0);
+        P xv[NP], dv[NP];
+        unpack2<T>(ok ? ld_shared_v4(stx + rr * RB + coff[j]) : make_uint4(0, 0, 0, 0), xv);
         unpack2<T>(ok ? ld_shared_v4(std_ + rr * RB + coff[j]) : make_uint4(0, 0, 0, 0), dv);
-        if constexpr (sizeof(T) == 2) {
-          // 16-bit x: the mixed-precision subtract (FHADD) expands and centres in one op
-          const uint32_t xw[4] = {xr.x, xr.y, xr.z, xr.w};
-#pragma unroll
-          for (int e = 0; e < NP; ++e)
-            xh[rr][j][e] = mul2(sub16x2_f32<T>(xw[e], -mcur[rr]), r2);
-        } else {
-          P xv[NP];
-          unpack2<T>(xr, xv);
-#pragma unroll
-          for (int e = 0; e < NP; ++e) xh[rr][j][e] = mul2(add2(xv[e], nm), r2);
-        }
 #pragma unroll
         for (int e = 0; e < NP; ++e) {
+          xh[rr][j][e] = mul2(add2(xv[e], nm), r2);
           gg[rr][j][e] = mul2(dv[e], s1[j][e]);
           sg[e & 1] = add2(sg[e & 1], gg[rr][j][e]);
           sgx[e & 1] = fma2(gg[rr][j][e], xh[rr][j][e], sgx[e & 1]);
