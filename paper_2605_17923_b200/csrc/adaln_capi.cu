@@ -200,6 +200,29 @@ const void* rows_kernel_pf(int dtype, int vi) {
   }
 }
 template <typename T>
+const void* rows_staged(int vi) {
+  switch (vi) {
+    case 0: return (const void*)al::adaln_fwd_rows<T, 1, true, false, true>;
+    case 1: return (const void*)al::adaln_fwd_rows<T, 2, true, false, true>;
+    case 2: return (const void*)al::adaln_fwd_rows<T, 3, true, false, true>;
+    case 3: return (const void*)al::adaln_fwd_rows<T, 4, true, false, true>;
+    case 4: return (const void*)al::adaln_fwd_rows<T, 6, true, false, true>;
+    case 5: return (const void*)al::adaln_fwd_rows<T, 8, true, false, true>;
+    case 6: return (const void*)al::adaln_fwd_rows<T, 12, true, false, true>;
+    case 7: return (const void*)al::adaln_fwd_rows<T, 16, true, false, true>;
+    case 8: return (const void*)al::adaln_fwd_rows<T, 20, true, false, true>;
+    default: return (const void*)al::adaln_fwd_rows<T, 24, true, false, true>;
+  }
+}
+const void* rows_staged_kernel(int dtype, int vi) {
+  switch (dtype) {
+    case AL_BF16: return rows_staged<__nv_bfloat16>(vi);
+    case AL_F16: return rows_staged<__half>(vi);
+    case AL_F64: return rows_staged<double>(vi);
+    default: return rows_staged<float>(vi);
+  }
+}
+template <typename T>
 const void* rows16(int vi) {
   switch (vi) {
     case 0: return (const void*)al::adaln_fwd_rows16<T, 1>;
@@ -340,16 +363,26 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
       pl.V = kVpl[vi];
       pl.threads = 256;
       pl.smem = 2 * static_cast<size_t>(D) * cs;
-      // variant 1 = keep packed (re-expand per pass), 2 = compiler's choice; default by width
-      // variant: 0 auto (16-bit rows -> mixed-precision single-pass kernel, else 1),
-      // 1 packed row, 2 compiler-expanded row, 3 packed row + bulk L2 prefetch of each warp's
-      // next row (slower on B200: 4.95 vs 5.53 TB/s at cfg2), 4 mixed-precision 16-bit kernel
+      // variant: 0 auto (= 1), 1 packed row, 2 compiler-expanded row, 3 packed row + bulk L2
+      // prefetch of each warp's next row (slower on B200: 4.95 vs 5.53 TB/s at cfg2),
+      // 4 mixed-precision 16-bit kernel, 5 packed row with a TMA-staged one-row lookahead per
+      // warp (16 warps, per-warp shared-memory row buffers)
       const bool is16 = dtype == AL_BF16 || dtype == AL_F16;
-      const bool mixed = is16 && (tu.variant == 0 || tu.variant == 4);
+      const bool mixed = is16 && tu.variant == 4;
       const bool repack = tu.variant != 2;
-      pl.R = mixed ? 2 : (repack ? 1 : 0);
-      pl.fn = mixed ? rows16_kernel(dtype, vi)
-                    : (tu.variant == 3 ? rows_kernel_pf(dtype, vi) : rows_kernel(dtype, vi, repack));
+      const size_t staged_smem = 2 * static_cast<size_t>(D) * cs + 16 * static_cast<size_t>(row_bytes) +
+                                 16 * sizeof(uint64_t) + 16;
+      const bool staged = tu.variant == 5 && staged_smem <= static_cast<size_t>(kSmemOptin);
+      pl.R = staged ? 3 : (mixed ? 2 : (repack ? 1 : 0));
+      if (staged) {
+        pl.threads = 512;
+        pl.smem = staged_smem;
+        pl.fn = rows_staged_kernel(dtype, vi);
+      } else {
+        pl.fn = mixed ? rows16_kernel(dtype, vi)
+                      : (tu.variant == 3 ? rows_kernel_pf(dtype, vi)
+                                         : rows_kernel(dtype, vi, repack));
+      }
     } else if (ring_plan(kernel, nvec, row_bytes, cs, tu, &pl)) {
       const bool full = kernel == 1 && nvec == static_cast<int64_t>(pl.V) * (pl.threads - 32);
       pl.fn = tma_kernel(kernel, dtype, pl.V, pl.R, full);
@@ -362,7 +395,7 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
         pl = Plan();
       } else {
         int64_t grid = static_cast<int64_t>(sms) * occ;
-        if (pl.path == 2) grid = std::min<int64_t>(grid, (N + 7) / 8);
+        if (pl.path == 2) grid = std::min<int64_t>(grid, (N + pl.threads / 32 - 1) / (pl.threads / 32));
         pl.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, grid)));
       }
     }
@@ -454,6 +487,8 @@ int al_device_init(int device) {
           rc = ensure_attr(rows_kernel(dt, vi, true), device);
           if (rc) return rc;
           rc = ensure_attr(rows_kernel_pf(dt, vi), device);
+          if (rc) return rc;
+          rc = ensure_attr(rows_staged_kernel(dt, vi), device);
           if (rc) return rc;
           if (dt == AL_BF16 || dt == AL_F16) {
             rc = ensure_attr(rows16_kernel(dt, vi), device);

@@ -126,8 +126,8 @@ struct StageWalker {
 // about half the registers -> twice the resident warps); false lets the compiler keep it
 // expanded.
 // =====================================================================================
-template <typename T, int VPL, bool PACKED, bool PREFETCH = false>
-__global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
+template <typename T, int VPL, bool PACKED, bool PREFETCH = false, bool STAGED = false>
+__global__ void __launch_bounds__(STAGED ? 512 : 256) adaln_fwd_rows(const FwdParams p) {
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
   constexpr int EPV = Traits<T>::EPV;
@@ -144,6 +144,25 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
   const CT eps = static_cast<CT>(p.eps);
   const int RB = p.row_bytes;
   bool nf = false;
+
+  // STAGED: each warp's next row is streamed by a 1-D TMA bulk copy into a private
+  // shared-memory row buffer while the current row is being computed (one-row lookahead per
+  // warp; the row itself still lives in registers for the three passes).
+  uint8_t* rowbuf = smem + 2 * static_cast<size_t>(p.nvec) * NP * sizeof(P) +
+                    static_cast<size_t>(warp) * RB;
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(smem + 2 * static_cast<size_t>(p.nvec) * NP *
+                                                          sizeof(P) +
+                                               static_cast<size_t>(nwarp) * RB) + warp;
+  uint32_t rph = 0;
+  uint64_t pol = 0;
+  if constexpr (STAGED) {
+    if (lane == 0) {
+      mbar_init(rbar, 1);
+      fence_mbar_init();
+      pol = policy_evict_first();
+    }
+    __syncwarp();
+  }
 
   // expand vector i of the row; with PACKED the expansion depends on the runtime zero z
   auto expand = [&](const uint4& raw, uint32_t z, P* q) {
@@ -172,15 +191,31 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
       }
     }
     __syncthreads();
+    if constexpr (STAGED) {
+      if (lane == 0 && row0 + warp < seg_end) {
+        mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(RB));
+        bulk_g2s(rowbuf, static_cast<const uint8_t*>(p.x) + (row0 + warp) * RB, RB, rbar, pol);
+      }
+    }
     for (int64_t row = row0 + warp; row < seg_end; row += nwarp) {
       const uint8_t* xr = static_cast<const uint8_t*>(p.x) + row * RB;
       // optional: warm L2 with this warp's next row (measured slower on B200: off by default)
       if (PREFETCH && lane == 0 && row + nwarp < seg_end) prefetch_l2_bulk(xr + nwarp * RB, RB);
       uint4 v[VPL];
+      if constexpr (STAGED) {
+        mbar_wait(rbar, rph);
+        rph ^= 1;
 #pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        const int c = lane + 32 * i;
-        v[i] = c < p.nvec ? ld_global_nc_v4(xr + c * 16) : make_uint4(0, 0, 0, 0);
+        for (int i = 0; i < VPL; ++i) {
+          const int c = lane + 32 * i;
+          v[i] = c < p.nvec ? ld_shared_v4(rowbuf + c * 16) : make_uint4(0, 0, 0, 0);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          const int c = lane + 32 * i;
+          v[i] = c < p.nvec ? ld_global_nc_v4(xr + c * 16) : make_uint4(0, 0, 0, 0);
+        }
       }
       // 32-bit/64-bit inputs: statistics of (x - K), K = the row's first element, so that rows
       // with a large common offset keep full precision in the fp32 sums (x - K is exact for
@@ -208,6 +243,15 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows(const FwdParams p) {
       }
       P t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
       const CT md = warp_sum(t.x + t.y) * invD;  // mean of (x - K)
+      if constexpr (STAGED) {
+        // every lane has consumed its share of the row buffer (pass 1 read all of v[] before
+        // the shuffles): hand the buffer back to the async proxy for the next row
+        if (lane == 0 && row + nwarp < seg_end) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(RB));
+          bulk_g2s(rowbuf, xr + static_cast<int64_t>(nwarp) * RB, RB, rbar, pol);
+        }
+      }
       const CT mean = K + md;
       const P nm = splat2(SHIFT ? -md : -mean);
       const uint32_t z1 = PACKED ? runtime_zero(md) : 0u;

@@ -526,3 +526,23 @@ def test_fused_stage2_matches_separate_kernel(cuda):
         assert max_rel_err(f64(u), f64(v)) <= 1e-6
     for u, v in zip(b, c):
         assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("dtype,shape", [(torch.bfloat16, (2, 700, 5120)),
+                                         (torch.float32, (3, 257, 1536)),
+                                         (torch.float16, (1, 300, 2048))])
+def test_forward_row_variants_agree(variant, dtype, shape, cuda):
+    b, s, d = shape
+    x, sc, sh, _ = make(b, s, d, dtype, cuda, seed=variant + 17)
+    yo, muo, rso = oracle.forward_batched(f64(x), f64(sc), f64(sh), 1e-6, threads=0)
+    try:
+        nat.set_tuning(0, variant=variant)
+        y, mu, rs = fused_forward(x, sc, sh)
+        y2, _, _ = fused_forward(x, sc, sh)
+    finally:
+        nat.set_tuning(0)
+    tol = {torch.float32: 1e-5, torch.bfloat16: 5e-3, torch.float16: 5e-3}[dtype]
+    assert max_rel_err(f64(y), yo) <= tol
+    assert max_rel_err(f64(rs), rso) <= 1e-5
+    assert torch.equal(y, y2)

@@ -67,7 +67,7 @@ def main():
                           "frac": round(gbs / peak, 4), "plan": plan}), flush=True)
 
     if "fwd" in args.which:
-        cfgs = [dict(variant=v) for v in (0, 1, 2, 3, 4)]
+        cfgs = [dict(variant=v) for v in (0, 1, 2, 3, 4, 5)]
         cfgs += [dict(V=V, R=R, smem=sm) for V, R, sm in itertools.product(
             (1, 2, 4), (1, 2, 4), (100 * 1024, 200 * 1024))]
         for c in cfgs:
