@@ -293,26 +293,50 @@ int occupancy(const Plan& pl, int dev, int* occ) {
 }
 
 // TMA-ring plan (wide forward or backward); returns false if the shape does not fit.
-bool ring_plan(int kernel, int64_t nvec, int row_bytes, int cs, const Tuning& tu, Plan* pl) {
+// The ring is sized per SM, not per CTA: with k CTAs resident per SM (limited by registers
+// and threads), each CTA gets ~kRingPerSm / k of shared memory, so narrow rows (small D, few
+// consumer warps per CTA) run several CTAs per SM instead of one CTA with an 8-deep ring.
+constexpr int kRingPerSm = 200 * 1024;
+
+bool ring_plan(int kernel, int dtype, int64_t nvec, int row_bytes, int cs, const Tuning& tu,
+               int dev, Plan* pl) {
   const int max_threads = kernel ? 384 : 512;  // __launch_bounds__ of the kernels
   const int vcap = kernel ? 352 : 256;
   int V = tu.V;
   if (V == 0) {
-    V = 4;
-    for (int v : {1, 2, 4})
-      if (((nvec + v - 1) / v + 31) / 32 * 32 <= vcap) {
-        V = v;
-        break;
-      }
+    if (kernel == 1) {
+      // backward: 2 vectors (16 columns) per thread amortise the per-row reductions best
+      V = nvec < 64 ? 1 : (((nvec + 1) / 2 + 31) / 32 * 32 <= vcap ? 2 : 4);
+    } else {
+      V = 4;
+      for (int v : {1, 2, 4})
+        if (((nvec + v - 1) / v + 31) / 32 * 32 <= vcap) {
+          V = v;
+          break;
+        }
+    }
   }
   const int64_t nc = ((nvec + V - 1) / V + 31) / 32 * 32;
   if (nc + 32 > max_threads) return false;
-  const int budget = tu.smem_budget ? tu.smem_budget : kDefaultBudget[kernel];
   int R = tu.R ? tu.R : kDefaultR[kernel];
   const int tensors = kernel ? 2 : 1;
   const int ncw = static_cast<int>(nc / 32);
+  const bool full = kernel == 1 && nvec == static_cast<int64_t>(V) * nc;
   while (true) {
     const int64_t stage = static_cast<int64_t>(tensors) * R * row_bytes;
+    const void* fn = tma_kernel(kernel, dtype, V, R, full);
+    int budget = tu.smem_budget;
+    if (budget == 0) {
+      int k_reg = 1;
+      if (ensure_attr(fn, dev) == AL_OK &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k_reg, fn, static_cast<int>(nc) + 32, 0) ==
+              cudaSuccess &&
+          k_reg >= 1) {
+        budget = std::max<int>(kRingPerSm / k_reg, static_cast<int>(3 * stage));
+      } else {
+        budget = kDefaultBudget[kernel];
+      }
+    }
     int64_t ns = budget / stage;
     if (ns > 8) ns = 8;
     if (ns < 2) ns = 2;
@@ -324,6 +348,7 @@ bool ring_plan(int kernel, int64_t nvec, int row_bytes, int cs, const Tuning& tu
       pl->NS = static_cast<int>(ns);
       pl->threads = static_cast<int>(nc) + 32;
       pl->smem = static_cast<size_t>(ns * stage) + extra;
+      pl->fn = fn;
       return true;
     }
     if (R == 1) return false;
@@ -383,9 +408,8 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
                       : (tu.variant == 3 ? rows_kernel_pf(dtype, vi)
                                          : rows_kernel(dtype, vi, repack));
       }
-    } else if (ring_plan(kernel, nvec, row_bytes, cs, tu, &pl)) {
-      const bool full = kernel == 1 && nvec == static_cast<int64_t>(pl.V) * (pl.threads - 32);
-      pl.fn = tma_kernel(kernel, dtype, pl.V, pl.R, full);
+    } else {
+      ring_plan(kernel, dtype, nvec, row_bytes, cs, tu, dev, &pl);
     }
     if (pl.path != 0) {
       int occ = 0;
