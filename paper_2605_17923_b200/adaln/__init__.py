@@ -9,7 +9,9 @@ Argument kinds:
   * torch CUDA tensors: computed in their own dtype (fp32/bf16/fp16 in fp32 arithmetic, fp64 in
     fp64), results stay on the device.  x may be [N, D] (reference) or [B, S, D] with per-sample
     scale/shift [B, D] (the north-star layout; dscale/dshift come back [B, D]).
-  * torch CPU tensors: copied to the current CUDA device, computed, copied back (same dtype).
+  * torch CPU tensors: streamed through the GPU in row chunks with host->device copies,
+    kernels and device->host copies overlapped on two streams (``_host.py``); results come
+    back in pinned host memory in the input dtype.
   * numpy arrays / sequences: the reference's semantics -- cast to float64 (``_as_f64``,
     adaln/__init__.py:81-85), computed in fp64 on the GPU, returned as float64 numpy arrays.
 
@@ -28,6 +30,7 @@ import numpy as np
 import torch
 
 from ..errors import InvalidTile, ShapeMismatch, StaleStats
+from ._host import host_backward, host_forward
 from ._ops import fused_backward, fused_forward, geometry, stat_dtype
 
 __all__ = [
@@ -125,6 +128,12 @@ def adaln_forward(x, scale, shift, eps: float = 1e-6, *, check_finite: bool = Tr
     Mirrors adaln/__init__.py:99-108 (errors: ShapeMismatch, NonFiniteInput, ValueError).
     """
     st = _Staged(x, scale, shift)
+    if st.kind == "torch-cpu":  # host buffers: chunked H2D / compute / D2H pipeline
+        geometry(x, scale, shift)
+        if eps <= 0:
+            raise ValueError("eps must be positive")
+        y, mu, rstd = host_forward(x, scale.to(x.dtype), shift.to(x.dtype), eps, True, st.device)
+        return AdalnOutput(y=y, mu=mu, rstd=rstd)
     xd, sc, sh = st.put(x), st.put(scale), st.put(shift)
     geometry(xd, sc, sh)  # ShapeMismatch before touching the GPU
     if eps <= 0:
@@ -144,20 +153,30 @@ def _check_cached(x: torch.Tensor, mu: torch.Tensor, rstd: torch.Tensor) -> None
                 f"rows {tuple(rows)}")
 
 
-def _backward(dy, x, scale, mu, rstd, d_tile: int, n_tile: int, check_finite: bool) -> AdalnGrads:
-    st = _Staged(dy, x, scale, mu, rstd)
-    dyd, xd, sc = st.put(dy), st.put(x), st.put(scale)
-    mud, rsd = st.put(mu), st.put(rstd)
-    if tuple(dyd.shape) != tuple(xd.shape):
-        raise ShapeMismatch(f"dy shape {tuple(dyd.shape)} != x shape {tuple(xd.shape)}")
-    g = geometry(xd, sc)
-    _check_cached(xd, mud, rsd)
+def _validate_backward(dy, x, scale, mu, rstd, d_tile: int, n_tile: int):
+    if tuple(dy.shape) != tuple(x.shape):
+        raise ShapeMismatch(f"dy shape {tuple(dy.shape)} != x shape {tuple(x.shape)}")
+    g = geometry(x, scale)
+    _check_cached(x, mu, rstd)
     if d_tile or n_tile:
         rows_per_group = g.seq if g.mod_stride else g.batch * g.seq
         if not (1 <= d_tile <= g.dim and 1 <= n_tile <= rows_per_group):
             raise InvalidTile(
                 f"tile config {TileConfig(d_tile, n_tile)} out of bounds for "
                 f"N={rows_per_group}, D={g.dim}")
+    return g
+
+
+def _backward(dy, x, scale, mu, rstd, d_tile: int, n_tile: int, check_finite: bool) -> AdalnGrads:
+    st = _Staged(dy, x, scale, mu, rstd)
+    if st.kind == "torch-cpu":  # host buffers: chunked H2D / compute / D2H pipeline
+        _validate_backward(dy, x, scale, mu, rstd, d_tile, n_tile)
+        dx, dscale, dshift = host_backward(dy.to(x.dtype), x, scale.to(x.dtype), mu, rstd,
+                                           d_tile, n_tile, True, st.device)
+        return AdalnGrads(dx=dx, dscale=dscale, dshift=dshift)
+    dyd, xd, sc = st.put(dy), st.put(x), st.put(scale)
+    mud, rsd = st.put(mu), st.put(rstd)
+    g = _validate_backward(dyd, xd, sc, mud, rsd, d_tile, n_tile)
     sdt = stat_dtype(xd.dtype)
     mud = mud.reshape(g.stats_shape).to(sdt)
     rsd = rsd.reshape(g.stats_shape).to(sdt)

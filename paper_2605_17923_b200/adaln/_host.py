@@ -1,0 +1,129 @@
+"""Host-buffer path: the reference-style call with torch CPU tensors, pipelined over row chunks.
+
+The reference API takes host arrays (adaln/__init__.py:99-158), so an end-to-end call moves
+every input over PCIe and every result back.  Done naively (copy in, compute, copy out) the two
+PCIe directions and the kernels serialise.  Here rows are processed in ~32 MB chunks: chunk i's
+inputs are copied in and computed on the current stream while chunk i-1's results drain to
+pinned host memory on a second stream, so host->device and device->host traffic overlap (they
+use different copy engines) and the kernels hide under the copies.
+
+Per-chunk dscale/dshift partials are summed in a fixed order in fp64 at the end, so results are
+deterministic for a given chunking.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from ..errors import NonFiniteInput
+from ._ops import fused_backward, fused_forward, geometry, stat_dtype
+
+CHUNK_BYTES = 32 << 20
+
+_side_streams: dict = {}
+
+
+def _side(dev: torch.device) -> torch.cuda.Stream:
+    s = _side_streams.get(dev.index)
+    if s is None:
+        s = _side_streams[dev.index] = torch.cuda.Stream(device=dev)
+    return s
+
+
+def _chunks(b: int, s: int, row_bytes: int):
+    """(b0, b1, s0, s1) blocks: whole samples when a sample is small, else row slices of one."""
+    rows = max(1, CHUNK_BYTES // max(row_bytes, 1))
+    if s >= rows:
+        for bi in range(b):
+            for s0 in range(0, s, rows):
+                yield bi, bi + 1, s0, min(s, s0 + rows)
+    else:
+        per = max(1, rows // max(s, 1))
+        for b0 in range(0, b, per):
+            yield b0, min(b, b0 + per), 0, s
+
+
+def _pinned_like(shape, dtype):
+    return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+
+def host_forward(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor, eps: float,
+                 check_finite: bool, dev: torch.device):
+    g = geometry(x, scale, shift)
+    B, S, D = g.batch, g.seq, g.dim
+    x3 = x.contiguous().view(B, S, D)
+    sdt = stat_dtype(x.dtype)
+    y = _pinned_like(x.shape, x.dtype)
+    mu = _pinned_like(g.stats_shape, sdt)
+    rs = _pinned_like(g.stats_shape, sdt)
+    y3, mu2, rs2 = y.view(B, S, D), mu.view(B, S), rs.view(B, S)
+    per_sample = g.mod_stride != 0
+    sc = scale.to(dev, non_blocking=True).to(x.dtype)
+    sh = shift.to(dev, non_blocking=True).to(x.dtype)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
+    main, side = torch.cuda.current_stream(dev), _side(dev)
+    for b0, b1, s0, s1 in _chunks(B, S, D * x.element_size()):
+        xd = x3[b0:b1, s0:s1].to(dev, non_blocking=True)
+        scb = sc[b0:b1] if per_sample else sc
+        shb = sh[b0:b1] if per_sample else sh
+        yd, mud, rsd = fused_forward(xd, scb, shb, eps, flag=flag)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            y3[b0:b1, s0:s1].copy_(yd, non_blocking=True)
+            mu2[b0:b1, s0:s1].copy_(mud, non_blocking=True)
+            rs2[b0:b1, s0:s1].copy_(rsd, non_blocking=True)
+        for t in (xd, yd, mud, rsd):
+            t.record_stream(side)
+    side.synchronize()
+    if flag is not None and int(flag.item()):
+        raise NonFiniteInput("x/scale/shift contains NaN or Inf")
+    return y, mu, rs
+
+
+def host_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mu: torch.Tensor,
+                  rstd: torch.Tensor, d_tile: int, n_tile: int, check_finite: bool,
+                  dev: torch.device):
+    g = geometry(x, scale)
+    B, S, D = g.batch, g.seq, g.dim
+    x3, dy3 = x.contiguous().view(B, S, D), dy.contiguous().view(B, S, D)
+    sdt = stat_dtype(x.dtype)
+    mu2 = mu.to(sdt).contiguous().view(B, S)
+    rs2 = rstd.to(sdt).contiguous().view(B, S)
+    dx = _pinned_like(x.shape, x.dtype)
+    dx3 = dx.view(B, S, D)
+    per_sample = g.mod_stride != 0
+    sc = scale.to(dev, non_blocking=True).to(x.dtype)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
+    main, side = torch.cuda.current_stream(dev), _side(dev)
+    parts = []  # (b0, b1, dscale chunk, dshift chunk) on the device
+    for b0, b1, s0, s1 in _chunks(B, S, 2 * D * x.element_size()):
+        xd = x3[b0:b1, s0:s1].to(dev, non_blocking=True)
+        dyd = dy3[b0:b1, s0:s1].to(dev, non_blocking=True)
+        mud = mu2[b0:b1, s0:s1].to(dev, non_blocking=True)
+        rsd = rs2[b0:b1, s0:s1].to(dev, non_blocking=True)
+        scb = sc[b0:b1] if per_sample else sc
+        nt = min(n_tile, (s1 - s0) if per_sample else (b1 - b0) * (s1 - s0)) if n_tile else 0
+        dxd, dsc, dsh = fused_backward(dyd, xd, scb, mud, rsd, d_tile=d_tile if nt else 0,
+                                       n_tile=nt, flag=flag)
+        parts.append((b0, b1, dsc, dsh))
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            dx3[b0:b1, s0:s1].copy_(dxd, non_blocking=True)
+        for t in (xd, dyd, mud, rsd, dxd):
+            t.record_stream(side)
+    # fixed-order fp64 sum of the chunk partials
+    acc_sc = torch.zeros((B, D) if per_sample else (D,), dtype=torch.float64, device=dev)
+    acc_sh = torch.zeros_like(acc_sc)
+    for b0, b1, dsc, dsh in parts:
+        if per_sample:
+            acc_sc[b0:b1] += dsc.double()
+            acc_sh[b0:b1] += dsh.double()
+        else:
+            acc_sc += dsc.double()
+            acc_sh += dsh.double()
+    dscale = acc_sc.to(sdt).cpu()
+    dshift = acc_sh.to(sdt).cpu()
+    side.synchronize()
+    if flag is not None and int(flag.item()):
+        raise NonFiniteInput("dy/x/scale contains NaN or Inf")
+    return dx, dscale, dshift

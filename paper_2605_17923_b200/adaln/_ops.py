@@ -87,8 +87,12 @@ def _raise_if_flagged(flag: torch.Tensor | None, what: str) -> None:
 
 
 def fused_forward(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor, eps: float = 1e-6,
-                  *, check_finite: bool = False, out: torch.Tensor | None = None):
-    """y, mean, rstd = AdaLN forward (one HBM pass).  Asynchronous unless check_finite."""
+                  *, check_finite: bool = False, out: torch.Tensor | None = None,
+                  flag: torch.Tensor | None = None):
+    """y, mean, rstd = AdaLN forward (one HBM pass).  Asynchronous unless check_finite.
+
+    ``flag`` (device int32[1]): accumulate the non-finite flag there without synchronising
+    (the caller checks it once, e.g. after a chunked host pipeline)."""
     if not x.is_cuda:
         raise ShapeMismatch("fused_forward takes CUDA tensors; use adaln_forward for host data")
     if eps <= 0:
@@ -103,19 +107,22 @@ def fused_forward(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor, eps
     sdt = stat_dtype(x.dtype)
     mean = torch.empty(g.stats_shape, dtype=sdt, device=dev)
     rstd = torch.empty(g.stats_shape, dtype=sdt, device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
+    own_flag = check_finite and flag is None
+    if own_flag:
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
     rc = nat.load().al_adaln_forward(
         x.data_ptr(), scale.data_ptr(), shift.data_ptr(), y.data_ptr(), mean.data_ptr(),
         rstd.data_ptr(), g.batch, g.seq, g.dim, g.mod_stride, dtype_code(x.dtype), float(eps),
         flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
     nat.check(rc, "al_adaln_forward")
-    _raise_if_flagged(flag, "x/scale/shift")
+    if own_flag:
+        _raise_if_flagged(flag, "x/scale/shift")
     return y, mean, rstd
 
 
 def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean: torch.Tensor,
                    rstd: torch.Tensor, *, d_tile: int = 0, n_tile: int = 0,
-                   check_finite: bool = False):
+                   check_finite: bool = False, flag: torch.Tensor | None = None):
     """dx, dscale, dshift in one pass over (dy, x) + a deterministic cross-CTA reduction."""
     if not x.is_cuda:
         raise ShapeMismatch("fused_backward takes CUDA tensors; use adaln_backward_* for host data")
@@ -140,12 +147,15 @@ def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean:
     dx = torch.empty_like(x)
     dscale = torch.empty(g.grad_shape, dtype=sdt, device=dev)
     dshift = torch.empty(g.grad_shape, dtype=sdt, device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
+    own_flag = check_finite and flag is None
+    if own_flag:
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
     rc = lib.al_adaln_backward(
         dy.data_ptr(), x.data_ptr(), scale.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
         dx.data_ptr(), dscale.data_ptr(), dshift.data_ptr(), ws.data_ptr(), int(ws_bytes),
         g.batch, g.seq, g.dim, g.mod_stride, code, d_tile, n_tile,
         flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
     nat.check(rc, "al_adaln_backward")
-    _raise_if_flagged(flag, "dy/x/scale")
+    if own_flag:
+        _raise_if_flagged(flag, "dy/x/scale")
     return dx, dscale, dshift

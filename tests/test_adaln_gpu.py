@@ -546,3 +546,29 @@ def test_forward_row_variants_agree(variant, dtype, shape, cuda):
     assert max_rel_err(f64(y), yo) <= tol
     assert max_rel_err(f64(rs), rso) <= 1e-5
     assert torch.equal(y, y2)
+
+
+@pytest.mark.parametrize("shape,mod", [((1, 70000, 1024), "per_sample"), ((5, 3000, 1536), "per_sample"),
+                                       ((40000, 512), "broadcast"), ((300, 64, 256), "per_sample")])
+def test_host_pipeline_matches_device_path(shape, mod, cuda):
+    """Chunked host-buffer path == device path (dx bitwise; reductions to fp32 resolution)."""
+    g = torch.Generator().manual_seed(3)
+    x = torch.randn(*shape, generator=g).to(torch.bfloat16)
+    dy = torch.randn(*shape, generator=g).to(torch.bfloat16)
+    d = shape[-1]
+    mshape = (shape[0], d) if mod == "per_sample" else (d,)
+    sc = (0.1 * torch.randn(*mshape, generator=g)).to(torch.bfloat16)
+    sh = (0.1 * torch.randn(*mshape, generator=g)).to(torch.bfloat16)
+    out = adaln_forward(x.pin_memory(), sc, sh)
+    ref = fused_forward(x.to(cuda), sc.to(cuda), sh.to(cuda))
+    assert out.y.device.type == "cpu" and out.y.is_pinned()
+    assert torch.equal(out.y, ref[0].cpu()) and torch.equal(out.rstd, ref[2].cpu())
+    gr = adaln_backward_naive(dy.pin_memory(), x.pin_memory(), sc, out.mu, out.rstd)
+    dref = fused_backward(dy.to(cuda), x.to(cuda), sc.to(cuda), ref[1], ref[2])
+    assert torch.equal(gr.dx, dref[0].cpu())
+    assert max_rel_err(f64(gr.dscale), f64(dref[1])) <= 1e-6
+    assert max_rel_err(f64(gr.dshift), f64(dref[2])) <= 1e-6
+    x_bad = x.clone()
+    x_bad.view(-1)[12345] = float("nan")
+    with pytest.raises(NonFiniteInput):
+        adaln_forward(x_bad, sc, sh)
