@@ -855,6 +855,9 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
     for (int rr = 0; rr < R; ++rr) {
       const bool live = rr < rows;
       const P nm = splat2(-mcur[rr]), r2 = splat2(rcur[rr]);
+      // 16-bit inputs: xhat = x*r - m*r in one FFMA2 (the product is exact inside the FMA;
+      // the absolute error ~|m| r 2^-24 is far below the inputs' own 2^-9 rounding)
+      const P nmr = splat2(-mcur[rr] * rcur[rr]);
       // two accumulators per row sum break the FADD2/FFMA2 dependency chains
       P sg[2] = {splat2(CT(0)), splat2(CT(0))}, sgx[2] = {splat2(CT(0)), splat2(CT(0))};
 #pragma unroll
@@ -865,7 +868,8 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
         unpack2<T>(ok ? ld_shared_v4(std_ + rr * RB + coff[j]) : make_uint4(0, 0, 0, 0), dv);
 #pragma unroll
         for (int e = 0; e < NP; ++e) {
-          xh[rr][j][e] = mul2(add2(xv[e], nm), r2);
+          if constexpr (sizeof(T) == 2) xh[rr][j][e] = fma2(xv[e], r2, nmr);
+          else xh[rr][j][e] = mul2(add2(xv[e], nm), r2);
           gg[rr][j][e] = mul2(dv[e], s1[j][e]);
           sg[e & 1] = add2(sg[e & 1], gg[rr][j][e]);
           sgx[e & 1] = fma2(gg[rr][j][e], xh[rr][j][e], sgx[e & 1]);
@@ -908,8 +912,10 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
     for (int rr = 0; rr < R; ++rr) {
       if (rr < rows) {
         const int64_t row = rb + rr;
-        const P nmg = splat2(-tot[2 * rr] * invD), nmgx = splat2(-tot[2 * rr + 1] * invD);
-        const P r2 = splat2(rcur[rr]);
+        // dx = r*g - r*mean(g) - (r*mean(g*xhat)) * xhat: two FFMA2 per pair
+        const CT rr_ = rcur[rr];
+        const P c0 = splat2(-rr_ * tot[2 * rr] * invD), c1 = splat2(-rr_ * tot[2 * rr + 1] * invD);
+        const P r2 = splat2(rr_);
         uint8_t* dxrow = static_cast<uint8_t*>(p.dx) + row * RB;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
@@ -917,7 +923,7 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
             P o[NP];
 #pragma unroll
             for (int e = 0; e < NP; ++e)
-              o[e] = mul2(fma2(xh[rr][j][e], nmgx, add2(gg[rr][j][e], nmg)), r2);
+              o[e] = fma2(gg[rr][j][e], r2, fma2(xh[rr][j][e], c1, c0));
             st_global_cs(dxrow + coff[j], pack2<T>(o));
           }
         }
