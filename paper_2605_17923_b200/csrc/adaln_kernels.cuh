@@ -891,20 +891,20 @@ __global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
-    // cross-warp totals (fixed warp order -> deterministic), 8/16-byte shared loads
-    P tot2[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) tot2[q] = splat2(CT(0));
-    for (int q = 0; q < ncw; ++q) {
-      const P* src = reinterpret_cast<const P*>(rd + q * 2 * R);
-#pragma unroll
-      for (int u = 0; u < R; ++u) tot2[u] = add2(tot2[u], src[u]);
-    }
+    // cross-warp totals, spread over the lanes: rd holds ncw x NV values [warp][k]; lane l
+    // sums entries l, l+32, ... (all of index k = l % NV), lanes of equal k are combined by a
+    // butterfly, and every thread then reads the NV totals by shuffles.  Fixed order ->
+    // deterministic; ~2 shared loads + 3 + NV shuffles instead of ncw * NV loads per thread.
     CT tot[2 * R];
+    {
+      constexpr int NV = 2 * R;
+      const int nval = ncw * NV;
+      CT s_l = CT(0);
+      for (int i = lane; i < nval; i += 32) s_l += rd[i];
 #pragma unroll
-    for (int u = 0; u < R; ++u) {
-      tot[2 * u] = tot2[u].x;
-      tot[2 * u + 1] = tot2[u].y;
+      for (int off = NV; off < 32; off <<= 1) s_l += __shfl_xor_sync(0xffffffffu, s_l, off);
+#pragma unroll
+      for (int q = 0; q < NV; ++q) tot[q] = __shfl_sync(0xffffffffu, s_l, q);
     }
 
     // phase 2: dx = rstd * (g - mean(g) - xhat * mean(g*xhat))
