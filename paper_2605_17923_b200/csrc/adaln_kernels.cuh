@@ -170,10 +170,25 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256) adaln_fwd_rows(const FwdPa
     else unpack2<T>(raw, q);
   };
 
+  uint4 v[VPL];
   int64_t row0 = r0;
   while (row0 < r1) {
     const int64_t g = row0 / p.S_grp;
     const int64_t seg_end = min(r1, (g + 1) * p.S_grp);
+    // issue this warp's first row of the segment before staging the modulation, so the HBM
+    // latency of the first row overlaps the CTA prologue
+    bool have_row = false;
+    if constexpr (!STAGED) {
+      if (row0 + warp < seg_end) {
+        const uint8_t* xr0 = static_cast<const uint8_t*>(p.x) + (row0 + warp) * RB;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          const int c = lane + 32 * i;
+          v[i] = c < p.nvec ? ld_global_nc_v4(xr0 + c * 16) : make_uint4(0, 0, 0, 0);
+        }
+        have_row = true;
+      }
+    }
     __syncthreads();  // every warp is done with the previous group's modulation
     {
       const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
@@ -201,7 +216,6 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256) adaln_fwd_rows(const FwdPa
       const uint8_t* xr = static_cast<const uint8_t*>(p.x) + row * RB;
       // optional: warm L2 with this warp's next row (measured slower on B200: off by default)
       if (PREFETCH && lane == 0 && row + nwarp < seg_end) prefetch_l2_bulk(xr + nwarp * RB, RB);
-      uint4 v[VPL];
       if constexpr (STAGED) {
         mbar_wait(rbar, rph);
         rph ^= 1;
@@ -210,6 +224,8 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256) adaln_fwd_rows(const FwdPa
           const int c = lane + 32 * i;
           v[i] = c < p.nvec ? ld_shared_v4(rowbuf + c * 16) : make_uint4(0, 0, 0, 0);
         }
+      } else if (have_row) {
+        have_row = false;  // first row of the segment: already in flight
       } else {
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
