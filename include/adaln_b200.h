@@ -62,7 +62,7 @@ extern "C" {
 #define AL_F16 2
 #define AL_F64 3
 
-/* ABI version of this header (bumped on any signature change). */
+/* ABI version of this header (bumped on any signature change or addition). */
 AL_API int al_abi_version(void);
 
 /* Human-readable message for the last error on the calling thread. */
@@ -80,6 +80,23 @@ AL_API int al_device_init(int device);
  */
 AL_API int al_adaln_forward(const void* x, const void* scale, const void* shift,
                      void* y, void* mean, void* rstd,
+                     int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
+                     int dtype, double eps, int* nonfinite, void* stream);
+
+/*
+ * Gated residual + forward, fused: the DiT block's
+ *     x_out = x + gate (.) f          gate per sample like scale/shift ([B, D] rows at mod_stride)
+ *     y, mean, rstd = AdaLN(x_out, scale, shift)
+ * in one pass (reads x, f; writes x_out, y, mean, rstd).  x_out is rounded to the storage dtype
+ * once (single fp32/fp64 fma), and the statistics are those of the rounded x_out, so y equals
+ * al_adaln_forward(x_out, ...) bit for bit.  The reference has no fused form: its block calls
+ * the residual add and `adaln_forward` separately (adaln/__init__.py:99-108 on the residual
+ * stream); gradients compose from al_adaln_backward (dx_out += dxn; df = gate * dx_out;
+ * dgate = sum_s f * dx_out).  x_out may not alias x or f.
+ */
+AL_API int al_adaln_gate_residual_forward(const void* x, const void* f, const void* gate,
+                     const void* scale, const void* shift,
+                     void* x_out, void* y, void* mean, void* rstd,
                      int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
                      int dtype, double eps, int* nonfinite, void* stream);
 

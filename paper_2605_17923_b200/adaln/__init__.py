@@ -31,7 +31,7 @@ import torch
 
 from ..errors import InvalidTile, ShapeMismatch, StaleStats
 from ._host import host_backward, host_forward
-from ._ops import fused_backward, fused_forward, geometry, stat_dtype
+from ._ops import fused_backward, fused_forward, fused_gate_residual_forward, geometry, stat_dtype  # noqa: F401
 
 __all__ = [
     "AdalnOutput",
@@ -217,4 +217,5 @@ def activation_bytes(n: int, d: int, element_bytes: int, stat_bytes: int, mode: 
 
 
 from ._gradcheck import DEFAULT_SIZES, GradcheckReport, gradcheck  # noqa: E402
-from .autograd import FusedAdaLNModulate, adaln_modulate  # noqa: E402,F401
+from .autograd import (FusedAdaLNModulate, FusedGateResidualAdaLN, adaln_modulate,  # noqa: E402,F401
+                       gate_residual_adaln)

@@ -120,6 +120,48 @@ def fused_forward(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor, eps
     return y, mean, rstd
 
 
+def fused_gate_residual_forward(x: torch.Tensor, f: torch.Tensor, gate: torch.Tensor,
+                                scale: torch.Tensor, shift: torch.Tensor, eps: float = 1e-6, *,
+                                check_finite: bool = False, flag: torch.Tensor | None = None):
+    """x_out = x + gate * f;  y, mean, rstd = AdaLN(x_out)  -- one pass (al_adaln_gate_residual_forward).
+
+    ``gate`` has the shape of scale/shift ([D] or [B, D]); returns (x_out, y, mean, rstd)."""
+    if not x.is_cuda:
+        raise ShapeMismatch("fused_gate_residual_forward takes CUDA tensors")
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    g = geometry(x, scale, shift)
+    geometry(x, gate)  # same broadcast rules as scale
+    if tuple(gate.shape) != tuple(scale.shape):
+        raise ShapeMismatch(f"gate shape {tuple(gate.shape)} != scale shape {tuple(scale.shape)}")
+    if tuple(f.shape) != tuple(x.shape):
+        raise ShapeMismatch(f"f shape {tuple(f.shape)} != x shape {tuple(x.shape)}")
+    dev = x.device
+    nat.ensure_device(dev.index)
+    x = _prep(x, x.dtype, dev)
+    f = _prep(f, x.dtype, dev)
+    gate = _prep(gate, x.dtype, dev)
+    scale = _prep(scale, x.dtype, dev)
+    shift = _prep(shift, x.dtype, dev)
+    x_out = torch.empty_like(x)
+    y = torch.empty_like(x)
+    sdt = stat_dtype(x.dtype)
+    mean = torch.empty(g.stats_shape, dtype=sdt, device=dev)
+    rstd = torch.empty(g.stats_shape, dtype=sdt, device=dev)
+    own_flag = check_finite and flag is None
+    if own_flag:
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    rc = nat.load().al_adaln_gate_residual_forward(
+        x.data_ptr(), f.data_ptr(), gate.data_ptr(), scale.data_ptr(), shift.data_ptr(),
+        x_out.data_ptr(), y.data_ptr(), mean.data_ptr(), rstd.data_ptr(), g.batch, g.seq, g.dim,
+        g.mod_stride, dtype_code(x.dtype), float(eps),
+        flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
+    nat.check(rc, "al_adaln_gate_residual_forward")
+    if own_flag:
+        _raise_if_flagged(flag, "x/f/gate/scale/shift")
+    return x_out, y, mean, rstd
+
+
 def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean: torch.Tensor,
                    rstd: torch.Tensor, *, d_tile: int = 0, n_tile: int = 0,
                    check_finite: bool = False, flag: torch.Tensor | None = None):

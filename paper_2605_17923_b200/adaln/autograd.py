@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import torch
 
-from ._ops import fused_backward, fused_forward
+from ._ops import fused_backward, fused_forward, fused_gate_residual_forward
 
 
 class FusedAdaLNModulate(torch.autograd.Function):
@@ -31,3 +31,40 @@ def adaln_modulate(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor,
                    eps: float = 1e-6) -> torch.Tensor:
     """y = LN(x) * (1 + scale) + shift with per-sample scale/shift [B, D] broadcast over S."""
     return FusedAdaLNModulate.apply(x, scale, shift, eps)
+
+
+class FusedGateResidualAdaLN(torch.autograd.Function):
+    """(x_out, y) = (x + gate * f, AdaLN(x + gate * f)) as one node (al_adaln_gate_residual_forward).
+
+    Saves x_out, f, gate, scale and the row statistics.  Backward, with upstream (g_xo, g_y):
+        G      = g_xo + dxn          dxn, dscale, dshift = fused AdaLN backward of g_y at x_out
+        dx     = G
+        df     = gate * G            (gate broadcast over the sequence)
+        dgate  = sum_s f * G         (fp32 accumulation)
+    """
+
+    @staticmethod
+    def forward(ctx, x, f, gate, scale, shift, eps: float = 1e-6):
+        x_out, y, mean, rstd = fused_gate_residual_forward(x, f, gate, scale, shift, eps)
+        ctx.save_for_backward(x_out, f, gate, scale, mean, rstd)
+        ctx.mod_dtypes = (gate.dtype, scale.dtype, shift.dtype)
+        return x_out, y
+
+    @staticmethod
+    def backward(ctx, g_xo, g_y):
+        x_out, f, gate, scale, mean, rstd = ctx.saved_tensors
+        # autograd materialises an unused output's gradient as zeros, so both are tensors here
+        dxn, dsc, dsh = fused_backward(g_y, x_out, scale, mean, rstd)
+        G = dxn + g_xo.to(dxn.dtype)
+        gb = gate.unsqueeze(-2) if gate.dim() == 2 and x_out.dim() == 3 else gate
+        df = G * gb.to(G.dtype)
+        red = tuple(range(x_out.dim() - 1)) if gate.dim() == 1 else (1,)
+        dgate = (f.float() * G.float()).sum(dim=red)
+        return (G, df, dgate.to(ctx.mod_dtypes[0]), dsc.to(ctx.mod_dtypes[1]),
+                dsh.to(ctx.mod_dtypes[2]), None)
+
+
+def gate_residual_adaln(x: torch.Tensor, f: torch.Tensor, gate: torch.Tensor, scale: torch.Tensor,
+                        shift: torch.Tensor, eps: float = 1e-6):
+    """(x + gate * f, LN(x + gate * f) * (1 + scale) + shift), fused forward, composed backward."""
+    return FusedGateResidualAdaLN.apply(x, f, gate, scale, shift, eps)

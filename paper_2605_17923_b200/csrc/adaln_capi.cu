@@ -237,6 +237,37 @@ const void* rows16(int vi) {
     default: return (const void*)al::adaln_fwd_rows16<T, 24>;
   }
 }
+template <typename T>
+const void* resid(int vi) {
+  switch (vi) {
+    case 0: return (const void*)al::adaln_fwd_rows<T, 1, true, false, false, true>;
+    case 1: return (const void*)al::adaln_fwd_rows<T, 2, true, false, false, true>;
+    case 2: return (const void*)al::adaln_fwd_rows<T, 3, true, false, false, true>;
+    case 3: return (const void*)al::adaln_fwd_rows<T, 4, true, false, false, true>;
+    case 4: return (const void*)al::adaln_fwd_rows<T, 6, true, false, false, true>;
+    case 5: return (const void*)al::adaln_fwd_rows<T, 8, true, false, false, true>;
+    case 6: return (const void*)al::adaln_fwd_rows<T, 12, true, false, false, true>;
+    case 7: return (const void*)al::adaln_fwd_rows<T, 16, true, false, false, true>;
+    case 8: return (const void*)al::adaln_fwd_rows<T, 20, true, false, false, true>;
+    default: return (const void*)al::adaln_fwd_rows<T, 24, true, false, false, true>;
+  }
+}
+const void* resid_kernel(int dtype, int vi) {
+  switch (dtype) {
+    case AL_BF16: return resid<__nv_bfloat16>(vi);
+    case AL_F16: return resid<__half>(vi);
+    case AL_F64: return resid<double>(vi);
+    default: return resid<float>(vi);
+  }
+}
+const void* resid_generic_kernel(int dtype) {
+  switch (dtype) {
+    case AL_BF16: return (const void*)al::gate_residual_generic<__nv_bfloat16>;
+    case AL_F16: return (const void*)al::gate_residual_generic<__half>;
+    case AL_F64: return (const void*)al::gate_residual_generic<double>;
+    default: return (const void*)al::gate_residual_generic<float>;
+  }
+}
 const void* rows16_kernel(int dtype, int vi) {
   return dtype == AL_BF16 ? rows16<__nv_bfloat16>(vi) : rows16<__half>(vi);
 }
@@ -466,11 +497,46 @@ int check_common(int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride, in
   return AL_OK;
 }
 
+al::FwdParams fwd_params(const void* x, const void* scale, const void* shift, void* y,
+                         void* mean, void* rstd, int64_t seq, int64_t N, int64_t dim,
+                         int64_t mod_stride, int dtype, double eps, int* nonfinite,
+                         const Plan& pl) {
+  al::FwdParams p;
+  p.x = x;
+  p.scale = scale;
+  p.shift = shift;
+  p.y = y;
+  p.mean = mean;
+  p.rstd = rstd;
+  p.N = N;
+  p.S_grp = mod_stride ? seq : N;
+  p.D = dim;
+  p.mod_stride = mod_stride;
+  p.eps = eps;
+  p.nonfinite = nonfinite;
+  p.nvec = static_cast<int>(dim * elem_size(dtype) / 16);
+  p.row_bytes = static_cast<int>(dim * elem_size(dtype));
+  p.nstages = pl.NS;
+  p.G = pl.grid;
+  p.f = nullptr;
+  p.gate = nullptr;
+  p.x_out = nullptr;
+  return p;
+}
+
+int launch(const Plan& pl, al::FwdParams& p, void* stream, const char* what) {
+  void* args[] = {&p};
+  cudaError_t e = cudaLaunchKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem,
+                                   static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  return AL_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
-int al_abi_version(void) { return 1; }
+int al_abi_version(void) { return 2; }
 
 const char* al_last_error(void) { return g_err; }
 
@@ -514,6 +580,8 @@ int al_device_init(int device) {
           if (rc) return rc;
           rc = ensure_attr(rows_staged_kernel(dt, vi), device);
           if (rc) return rc;
+          rc = ensure_attr(resid_kernel(dt, vi), device);
+          if (rc) return rc;
           if (dt == AL_BF16 || dt == AL_F16) {
             rc = ensure_attr(rows16_kernel(dt, vi), device);
             if (rc) return rc;
@@ -521,6 +589,11 @@ int al_device_init(int device) {
         }
       cudaFuncAttributes fa;
       e = cudaFuncGetAttributes(&fa, generic_kernel(kernel, dt));
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+    }
+    {
+      cudaFuncAttributes fa;
+      e = cudaFuncGetAttributes(&fa, resid_generic_kernel(dt));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
     }
     for (bool vec : {false, true}) {
@@ -565,28 +638,73 @@ int al_adaln_forward(const void* x, const void* scale, const void* shift, void* 
   Plan pl;
   rc = make_plan(0, N, dim, mod_stride, dtype, 0, vp, 4, &pl);
   if (rc) return rc;
-  al::FwdParams p;
-  p.x = x;
-  p.scale = scale;
-  p.shift = shift;
-  p.y = y;
-  p.mean = mean;
-  p.rstd = rstd;
-  p.N = N;
-  p.S_grp = mod_stride ? seq : N;
-  p.D = dim;
-  p.mod_stride = mod_stride;
-  p.eps = eps;
-  p.nonfinite = nonfinite;
-  p.nvec = static_cast<int>(dim * elem_size(dtype) / 16);
-  p.row_bytes = static_cast<int>(dim * elem_size(dtype));
-  p.nstages = pl.NS;
-  p.G = pl.grid;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  void* args[] = {&p};
-  cudaError_t e = cudaLaunchKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st);
-  if (e != cudaSuccess) return cuda_fail(e, "forward launch");
-  return AL_OK;
+  al::FwdParams p = fwd_params(x, scale, shift, y, mean, rstd, seq, N, dim, mod_stride, dtype,
+                               eps, nonfinite, pl);
+  return launch(pl, p, stream, "forward launch");
+}
+
+int al_adaln_gate_residual_forward(const void* x, const void* f, const void* gate,
+                                   const void* scale, const void* shift, void* x_out, void* y,
+                                   void* mean, void* rstd, int64_t batch, int64_t seq,
+                                   int64_t dim, int64_t mod_stride, int dtype, double eps,
+                                   int* nonfinite, void* stream) {
+  int rc = check_common(batch, seq, dim, mod_stride, dtype);
+  if (rc) return rc;
+  if (!(eps > 0.0)) return fail(AL_ERR_VALUE, "eps must be positive");
+  const int64_t N = batch * seq;
+  if (N == 0) return AL_OK;
+  if (!x || !f || !gate || !scale || !shift || !x_out || !y || !mean || !rstd)
+    return fail(AL_ERR_SHAPE, "null tensor pointer");
+  if (x_out == x || x_out == f) return fail(AL_ERR_VALUE, "x_out may not alias x or f");
+  const void* vp[7] = {x, f, gate, x_out, y, scale, shift};
+  Plan pl;
+  rc = make_plan(0, N, dim, mod_stride, dtype, 0, vp, 7, &pl);
+  if (rc) return rc;
+  if (pl.path == 2) {
+    // fused: swap the rows kernel for its gated-residual twin (same geometry, +1 smem row)
+    int vi = 0;
+    while (kVpl[vi] < pl.V) ++vi;
+    Plan pr = pl;
+    pr.fn = resid_kernel(dtype, vi);
+    pr.threads = 256;
+    pr.smem = 3 * static_cast<size_t>(dim) * ct_size(dtype);
+    int dev, sms, occ = 0;
+    rc = current_device(&dev);
+    if (!rc) rc = dev_sms(dev, &sms);
+    if (!rc) rc = occupancy(pr, dev, &occ);
+    if (rc) return rc;
+    if (occ >= 1) {
+      const int64_t grid = std::min<int64_t>(static_cast<int64_t>(sms) * occ, (N + 7) / 8);
+      pr.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, grid)));
+      al::FwdParams p = fwd_params(x, scale, shift, y, mean, rstd, seq, N, dim, mod_stride,
+                                   dtype, eps, nonfinite, pr);
+      p.f = f;
+      p.gate = gate;
+      p.x_out = x_out;
+      return launch(pr, p, stream, "gate-residual forward launch");
+    }
+  }
+  // unfused: residual kernel, then the forward plan on x_out
+  {
+    int dev, sms;
+    rc = current_device(&dev);
+    if (!rc) rc = dev_sms(dev, &sms);
+    if (rc) return rc;
+    Plan pg;
+    pg.threads = 256;
+    pg.fn = resid_generic_kernel(dtype);
+    pg.grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>((N * dim + 255) / 256, static_cast<int64_t>(sms) * 8)));
+    al::FwdParams p = fwd_params(x, scale, shift, y, mean, rstd, seq, N, dim, mod_stride, dtype,
+                                 eps, nonfinite, pg);
+    p.f = f;
+    p.gate = gate;
+    p.x_out = x_out;
+    rc = launch(pg, p, stream, "gate-residual launch");
+    if (rc) return rc;
+  }
+  return al_adaln_forward(x_out, scale, shift, y, mean, rstd, batch, seq, dim, mod_stride, dtype,
+                          eps, nonfinite, stream);
 }
 
 int64_t al_adaln_backward_workspace_bytes(int64_t batch, int64_t seq, int64_t dim,

@@ -50,6 +50,10 @@ struct FwdParams {
   int row_bytes;  // D * sizeof(T)
   int nstages;    // ring depth
   int G;          // CTAs
+  // gated-residual fusion (adaln_fwd_rows<..., RESID>): x_out = x + gate * f, y = AdaLN(x_out)
+  const void* f;
+  const void* gate;
+  void* x_out;
 };
 
 struct BwdParams {
@@ -126,8 +130,18 @@ struct StageWalker {
 // about half the registers -> twice the resident warps); false lets the compiler keep it
 // expanded.
 // =====================================================================================
-template <typename T, int VPL, bool PACKED, bool PREFETCH = false, bool STAGED = false>
-__global__ void __launch_bounds__(STAGED ? 512 : 256) adaln_fwd_rows(const FwdParams p) {
+//
+// RESID: the gated-residual twin (the DiT block's "x + gate * f -> norm"):
+//   x_out = x + gate (.) f   (gate per sample like scale/shift; one fp32/fp64 fma, rounded to T)
+//   y     = AdaLN(x_out)     (statistics of the rounded x_out: y is bit-identical to the plain
+//                             kernel applied to x_out)
+// reads x and f, writes x_out and y (+ mean, rstd): 4 N*D element moves where the unfused pair
+// (residual add, then the norm) moves 5 (7 with an eager mul + add).  x_out is stored in
+// pass 3 next to y, so no store sits between the row loads.
+template <typename T, int VPL, bool PACKED, bool PREFETCH = false, bool STAGED = false,
+          bool RESID = false>
+__global__ void __launch_bounds__(STAGED ? 512 : 256, RESID ? 2 : 1) adaln_fwd_rows(const FwdParams p) {
+  static_assert(!(RESID && STAGED), "the gated residual is not staged");
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
   constexpr int EPV = Traits<T>::EPV;
@@ -136,6 +150,7 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256) adaln_fwd_rows(const FwdPa
   extern __shared__ __align__(16) uint8_t smem[];
   P* s1 = reinterpret_cast<P*>(smem);  // [nvec * NP] : 1 + scale
   P* sh = s1 + p.nvec * NP;            // [nvec * NP] : shift
+  P* gt = sh + p.nvec * NP;            // [nvec * NP] : gate (RESID only)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   const int64_t k = blockIdx.x;
@@ -178,7 +193,7 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256) adaln_fwd_rows(const FwdPa
     // issue this warp's first row of the segment before staging the modulation, so the HBM
     // latency of the first row overlaps the CTA prologue
     bool have_row = false;
-    if constexpr (!STAGED) {
+    if constexpr (!STAGED && !RESID) {
       if (row0 + warp < seg_end) {
         const uint8_t* xr0 = static_cast<const uint8_t*>(p.x) + (row0 + warp) * RB;
 #pragma unroll
@@ -193,6 +208,7 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256) adaln_fwd_rows(const FwdPa
     {
       const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
       const uint8_t* sf = static_cast<const uint8_t*>(p.shift) + g * p.mod_stride * sizeof(T);
+      const uint8_t* ga = static_cast<const uint8_t*>(p.gate) + g * p.mod_stride * sizeof(T);
       for (int c = tid; c < p.nvec; c += blockDim.x) {
         P a[NP], b[NP];
         unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sc) + c), a);
@@ -202,6 +218,14 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256) adaln_fwd_rows(const FwdPa
           nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y) && finite_ct(b[e].x) && finite_ct(b[e].y));
           s1[c * NP + e] = add2(a[e], splat2(CT(1)));
           sh[c * NP + e] = b[e];
+        }
+        if constexpr (RESID) {
+          unpack2<T>(__ldg(reinterpret_cast<const uint4*>(ga) + c), a);
+#pragma unroll
+          for (int e = 0; e < NP; ++e) {
+            nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y));
+            gt[c * NP + e] = a[e];
+          }
         }
       }
     }
@@ -226,6 +250,29 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256) adaln_fwd_rows(const FwdPa
         }
       } else if (have_row) {
         have_row = false;  // first row of the segment: already in flight
+      } else if constexpr (RESID) {
+        // branch-free (predicated loads, clamped smem index): x lands in v[] exactly as in the
+        // plain kernel, then f streams in and is folded in place, so at most one row of x plus
+        // the in-flight f vectors are live (fits 128 registers -> 16 warps per SM)
+        const uint8_t* fr = static_cast<const uint8_t*>(p.f) + row * RB;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          const int c = lane + 32 * i;
+          v[i] = c < p.nvec ? ld_global_nc_v4(xr + c * 16) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          const int c = lane + 32 * i;
+          const bool ok = c < p.nvec;
+          const int cc = ok ? c : 0;
+          const uint4 fw = ok ? ld_global_nc_v4(fr + c * 16) : make_uint4(0, 0, 0, 0);
+          P xa[NP], fa[NP];
+          unpack2<T>(v[i], xa);
+          unpack2<T>(fw, fa);
+#pragma unroll
+          for (int e = 0; e < NP; ++e) xa[e] = fma2(gt[cc * NP + e], fa[e], xa[e]);
+          v[i] = pack2<T>(xa);
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
@@ -297,6 +344,7 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256) adaln_fwd_rows(const FwdPa
       for (int i = 0; i < VPL; ++i) {
         const int c = lane + 32 * i;
         if (c < p.nvec) {
+          if constexpr (RESID) st_global_cs(static_cast<uint8_t*>(p.x_out) + row * RB + c * 16, v[i]);
           P q[NP], a[NP], b[NP];
           expand(v[i], z2, q);
 #pragma unroll
@@ -1118,6 +1166,29 @@ __global__ void __launch_bounds__(256) adaln_fwd_generic(const FwdParams p) {
       static_cast<CT*>(p.rstd)[row] = rs;
       nf |= !(finite_ct(mean) && finite_ct(m2));
     }
+  }
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+// Gated residual for shapes the fused kernel does not take (unaligned pointers, wide rows):
+// x_out = x + gate (.) f with the same single fp32 (fp64) rounding; adaln_fwd_generic/wide then
+// normalises x_out.
+template <typename T>
+__global__ void __launch_bounds__(256) gate_residual_generic(const FwdParams p) {
+  using CT = typename Traits<T>::CT;
+  const T* x = static_cast<const T*>(p.x);
+  const T* f = static_cast<const T*>(p.f);
+  const T* ga = static_cast<const T*>(p.gate);
+  T* xo = static_cast<T*>(p.x_out);
+  const int64_t total = p.N * p.D;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  bool nf = false;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += stride) {
+    const int64_t row = i / p.D, j = i - row * p.D;
+    const CT g = to_ct(ga[(row / p.S_grp) * p.mod_stride + j]);
+    nf |= !finite_ct(g);
+    xo[i] = from_ct<T>(fma(g, to_ct(f[i]), to_ct(x[i])));
   }
   if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
 }

@@ -56,7 +56,8 @@ class WanStyleBlock(nn.Module):
 
     ``norm_fn(x, scale, shift, eps)`` is the fused LayerNorm-Modulate; the default is the
     sm_100a kernel pair (``adaln_modulate``).  Tests may inject a CPU stand-in to exercise the
-    data-parallel host logic on gloo.
+    data-parallel host logic on gloo.  With the default norm the attention residual and the
+    second norm run as ONE fused kernel (``gate_residual_adaln``: x + gate1 * proj(a) -> AdaLN).
     """
 
     def __init__(self, cfg: BlockConfig = BlockConfig(), norm_fn=None):
@@ -71,10 +72,12 @@ class WanStyleBlock(nn.Module):
         self.proj = nn.Linear(d, d)
         self.ffn_in = nn.Linear(d, cfg.ffn)
         self.ffn_out = nn.Linear(cfg.ffn, d)
+        self.resid_norm_fn = None
         if norm_fn is None:
-            from .adaln import adaln_modulate
+            from .adaln import adaln_modulate, gate_residual_adaln
 
             norm_fn = adaln_modulate
+            self.resid_norm_fn = gate_residual_adaln
         self.norm_fn = norm_fn
 
     def forward(self, x: torch.Tensor, t_emb: torch.Tensor) -> torch.Tensor:
@@ -88,8 +91,12 @@ class WanStyleBlock(nn.Module):
         k = self.k_norm(k).to(v.dtype).transpose(1, 2)
         v = v.transpose(1, 2)
         a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(b, s, d)
-        x = x + self.proj(a) * gate1[:, None, :]
-        y = self.norm_fn(x, scale2.contiguous(), shift2.contiguous(), self.cfg.eps)
+        if self.resid_norm_fn is not None:
+            x, y = self.resid_norm_fn(x, self.proj(a), gate1.contiguous(), scale2.contiguous(),
+                                      shift2.contiguous(), self.cfg.eps)
+        else:
+            x = x + self.proj(a) * gate1[:, None, :]
+            y = self.norm_fn(x, scale2.contiguous(), shift2.contiguous(), self.cfg.eps)
         x = x + self.ffn_out(F.gelu(self.ffn_in(y), approximate="tanh")) * gate2[:, None, :]
         return x
 
