@@ -15,6 +15,9 @@ from pathlib import Path
 from .errors import InvalidTile, NativeLibraryError, ShapeMismatch
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libadaln_b200.so"
+# A/B hook for kernel experiments (tools/ab_variant.sh): load another in-tree build instead
+if os.environ.get("AL_LIB_VARIANT"):
+    LIB_PATH = LIB_PATH.parent / "variants" / (os.environ["AL_LIB_VARIANT"] + ".so")
 
 AL_OK = 0
 AL_ERR_SHAPE = 1

@@ -92,4 +92,13 @@ __device__ __forceinline__ uint4 ld_shared_v4(const void* p) {
   return v;
 }
 
+// 32-bit shared-window address form: no generic->shared conversion per access.
+__device__ __forceinline__ uint4 ld_shared_v4_u32(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
+}
+
 }  // namespace al
