@@ -128,7 +128,7 @@ AL_API int al_adaln_backward(const void* dy, const void* x, const void* scale,
  * vecs_per_thread in {1,2,4}; rows_per_stage in {1,2,4}; smem_budget in bytes per CTA;
  * force_generic = 1 routes through the generic (any-shape) kernels.  variant: forward -- the rows
  * kernel flavour (0 auto, 1 packed row, 2 compiler-expanded row, 3 packed + L2 prefetch,
- * 4 mixed-precision 16-bit); backward -- 0 separate stage-2 kernel, 2 stage 2 fused into the
+ * 4 mixed-precision 16-bit, 5 TMA-staged lookahead, 6 two rows per warp); backward -- 0 separate stage-2 kernel, 2 stage 2 fused into the
  * stage-1 kernel behind a cooperative grid barrier.  Process-global.  For the forward kernel a nonzero
  * vecs_per_thread / rows_per_stage selects the wide (TMA ring) path.
  */
@@ -137,8 +137,8 @@ AL_API int al_set_tuning(int kernel, int vecs_per_thread, int rows_per_stage, in
 
 /* Describe the launch al_adaln_{forward,backward} would use: writes
  * {path (0 generic, 1 TMA ring, 2 rows-in-registers), grid, threads, vecs_per_thread (rows
- * path: 16-byte vectors per lane), rows_per_stage (rows path: 1 if the re-expanding variant),
- * stages, smem_bytes}. */
+ * path: 16-byte vectors per lane), rows_per_stage (rows path: the kernel flavour -- 0 expanded,
+ * 1 packed, 2 mixed 16-bit, 3 staged, 4 two rows per warp), stages, smem_bytes}. */
 AL_API int al_describe_launch(int kernel, int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
                        int dtype, int64_t n_tile, int64_t out[7]);
 

@@ -252,6 +252,29 @@ const void* resid(int vi) {
     default: return (const void*)al::adaln_fwd_rows<T, 24, true, false, false, true>;
   }
 }
+template <typename T>
+const void* rows2(int vi) {
+  switch (vi) {
+    case 0: return (const void*)al::adaln_fwd_rows2<T, 1>;
+    case 1: return (const void*)al::adaln_fwd_rows2<T, 2>;
+    case 2: return (const void*)al::adaln_fwd_rows2<T, 3>;
+    case 3: return (const void*)al::adaln_fwd_rows2<T, 4>;
+    case 4: return (const void*)al::adaln_fwd_rows2<T, 6>;
+    case 5: return (const void*)al::adaln_fwd_rows2<T, 8>;
+    case 6: return (const void*)al::adaln_fwd_rows2<T, 12>;
+    case 7: return (const void*)al::adaln_fwd_rows2<T, 16>;
+    case 8: return (const void*)al::adaln_fwd_rows2<T, 20>;
+    default: return (const void*)al::adaln_fwd_rows2<T, 24>;
+  }
+}
+const void* rows2_kernel(int dtype, int vi) {
+  switch (dtype) {
+    case AL_BF16: return rows2<__nv_bfloat16>(vi);
+    case AL_F16: return rows2<__half>(vi);
+    case AL_F64: return rows2<double>(vi);
+    default: return rows2<float>(vi);
+  }
+}
 const void* resid_kernel(int dtype, int vi) {
   switch (dtype) {
     case AL_BF16: return resid<__nv_bfloat16>(vi);
@@ -331,9 +354,10 @@ constexpr int kRingPerSm = 200 * 1024;
 
 bool ring_plan(int kernel, int dtype, int64_t nvec, int row_bytes, int cs, const Tuning& tu,
                int dev, Plan* pl) {
-  const int max_threads = kernel ? 384 : 512;  // __launch_bounds__ of the kernels
-  const int vcap = kernel ? 352 : 256;
   int V = tu.V;
+  // __launch_bounds__ of the kernels: backward V=1 takes up to 21 consumer warps (<= 93 regs)
+  const int max_threads = kernel ? (V == 1 ? 704 : 384) : 512;
+  const int vcap = kernel ? 352 : 256;
   if (V == 0) {
     if (kernel == 1) {
       // backward: 2 vectors (16 columns) per thread amortise the per-row reductions best
@@ -419,25 +443,42 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
       pl.V = kVpl[vi];
       pl.threads = 256;
       pl.smem = 2 * static_cast<size_t>(D) * cs;
-      // variant: 0 auto (= 1), 1 packed row, 2 compiler-expanded row, 3 packed row + bulk L2
-      // prefetch of each warp's next row (slower on B200: 4.95 vs 5.53 TB/s at cfg2),
-      // 4 mixed-precision 16-bit kernel, 5 packed row with a TMA-staged one-row lookahead per
-      // warp (16 warps, per-warp shared-memory row buffers)
+      // variant: 1 packed row, 2 compiler-expanded row, 3 packed row + bulk L2 prefetch of
+      // each warp's next row (slower on B200: 4.95 vs 5.53 TB/s at cfg2), 4 mixed-precision
+      // 16-bit kernel, 5 packed row with a TMA-staged one-row lookahead per warp, 6 two rows
+      // per warp.  0 = auto, from the B200 sweeps (profiles/r1_fwd_variants.jsonl):
+      //   16-bit, <= 6 vectors per lane (D <= 1536 bf16) -> 6  (+4..15 %: half the LDS traffic)
+      //   16-bit, 8..16 vectors, or short CTA ranges    -> 4  (+2..14 %)
+      //   otherwise (wide 16-bit rows with long ranges; fp32/fp64) -> 1
       const bool is16 = dtype == AL_BF16 || dtype == AL_F16;
-      const bool mixed = is16 && tu.variant == 4;
-      const bool repack = tu.variant != 2;
+      int variant = tu.variant;
+      if (variant == 0) {
+        variant = 1;
+        if (is16) {
+          const int64_t rows_per_cta = N / (2 * static_cast<int64_t>(sms));
+          if (kVpl[vi] <= 6) variant = 6;
+          else if (kVpl[vi] <= 16 || rows_per_cta < 64) variant = 4;
+        }
+      }
+      const bool mixed = is16 && variant == 4;
+      const bool repack = variant != 2;
       const size_t staged_smem = 2 * static_cast<size_t>(D) * cs + 16 * static_cast<size_t>(row_bytes) +
                                  16 * sizeof(uint64_t) + 16;
-      const bool staged = tu.variant == 5 && staged_smem <= static_cast<size_t>(kSmemOptin);
+      const bool staged = variant == 5 && staged_smem <= static_cast<size_t>(kSmemOptin);
+      // describe_launch "R" for the rows path: 0 expanded, 1 packed, 2 mixed 16-bit,
+      // 3 staged, 4 two rows per warp
       pl.R = staged ? 3 : (mixed ? 2 : (repack ? 1 : 0));
       if (staged) {
         pl.threads = 512;
         pl.smem = staged_smem;
         pl.fn = rows_staged_kernel(dtype, vi);
+      } else if (variant == 6) {
+        pl.R = 4;
+        pl.fn = rows2_kernel(dtype, vi);
       } else {
         pl.fn = mixed ? rows16_kernel(dtype, vi)
-                      : (tu.variant == 3 ? rows_kernel_pf(dtype, vi)
-                                         : rows_kernel(dtype, vi, repack));
+                      : (variant == 3 ? rows_kernel_pf(dtype, vi)
+                                      : rows_kernel(dtype, vi, repack));
       }
     } else {
       ring_plan(kernel, dtype, nvec, row_bytes, cs, tu, dev, &pl);
@@ -450,7 +491,10 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
         pl = Plan();
       } else {
         int64_t grid = static_cast<int64_t>(sms) * occ;
-        if (pl.path == 2) grid = std::min<int64_t>(grid, (N + pl.threads / 32 - 1) / (pl.threads / 32));
+        if (pl.path == 2) {
+          const int64_t rows_per_cta = static_cast<int64_t>(pl.threads / 32) * (pl.R == 4 ? 2 : 1);
+          grid = std::min<int64_t>(grid, (N + rows_per_cta - 1) / rows_per_cta);
+        }
         pl.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, grid)));
       }
     }
@@ -581,6 +625,8 @@ int al_device_init(int device) {
           rc = ensure_attr(rows_staged_kernel(dt, vi), device);
           if (rc) return rc;
           rc = ensure_attr(resid_kernel(dt, vi), device);
+          if (rc) return rc;
+          rc = ensure_attr(rows2_kernel(dt, vi), device);
           if (rc) return rc;
           if (dt == AL_BF16 || dt == AL_F16) {
             rc = ensure_attr(rows16_kernel(dt, vi), device);

@@ -372,6 +372,172 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256, RESID ? 2 : 0) adaln_fwd_r
 }
 
 // =====================================================================================
+// Forward, two rows per warp (variant 6).  Like adaln_fwd_rows<PACKED> but each warp holds
+// rows (r, r+1) at once: every (1+scale, shift) shared-memory read feeds two rows (half the
+// LDS traffic -- the forward's top stall is short_scoreboard on those reads), the two row
+// statistics share one reduce-scatter, and the per-row loop overhead halves.  Twice the
+// registers per warp, half the warps: the same bytes in flight per SM.
+// =====================================================================================
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256) adaln_fwd_rows2(const FwdParams p) {
+  using CT = typename Traits<T>::CT;
+  using P = typename PairOf<CT>::type;
+  constexpr int EPV = Traits<T>::EPV;
+  constexpr int NP = EPV / 2;
+  constexpr bool SHIFT = sizeof(T) >= 4;
+  extern __shared__ __align__(16) uint8_t smem[];
+  P* s1 = reinterpret_cast<P*>(smem);
+  P* sh = s1 + p.nvec * NP;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+  const CT invD = CT(1) / static_cast<CT>(p.D);
+  const CT eps = static_cast<CT>(p.eps);
+  const int RB = p.row_bytes;
+  bool nf = false;
+
+  uint4 v[2][VPL];
+  int64_t row0 = r0;
+  while (row0 < r1) {
+    const int64_t g = row0 / p.S_grp;
+    const int64_t seg_end = min(r1, (g + 1) * p.S_grp);
+    __syncthreads();
+    {
+      const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
+      const uint8_t* sf = static_cast<const uint8_t*>(p.shift) + g * p.mod_stride * sizeof(T);
+      for (int c = tid; c < p.nvec; c += blockDim.x) {
+        P a[NP], b[NP];
+        unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sc) + c), a);
+        unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sf) + c), b);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y) && finite_ct(b[e].x) && finite_ct(b[e].y));
+          s1[c * NP + e] = add2(a[e], splat2(CT(1)));
+          sh[c * NP + e] = b[e];
+        }
+      }
+    }
+    __syncthreads();
+    for (int64_t row = row0 + 2 * warp; row < seg_end; row += 2 * nwarp) {
+      const bool two = row + 1 < seg_end;
+      const uint8_t* xr = static_cast<const uint8_t*>(p.x) + row * RB;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        v[0][i] = c < p.nvec ? ld_global_nc_v4(xr + c * 16) : make_uint4(0, 0, 0, 0);
+        v[1][i] = (two && c < p.nvec) ? ld_global_nc_v4(xr + RB + c * 16) : make_uint4(0, 0, 0, 0);
+      }
+      CT K[2] = {CT(0), CT(0)};
+      if constexpr (SHIFT) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          P q0[NP];
+          unpack2<T>(v[q][0], q0);
+          K[q] = __shfl_sync(0xffffffffu, q0[0].x, 0);
+        }
+      }
+      // pass 1: means
+      CT part[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const P nK = splat2(-K[q]);
+        P acc[4] = {splat2(CT(0)), splat2(CT(0)), splat2(CT(0)), splat2(CT(0))};
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          if (!SHIFT || lane + 32 * i < p.nvec) {
+            P t[NP];
+            unpack2_dep<T>(v[q][i], 0u, t);
+#pragma unroll
+            for (int e = 0; e < NP; ++e)
+              acc[(i * NP + e) & 3] = add2(acc[(i * NP + e) & 3], SHIFT ? add2(t[e], nK) : t[e]);
+          }
+        }
+        const P t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+        part[q] = t.x + t.y;
+      }
+      CT md[2];
+      {
+        const CT u = warp_reduce_scatter<2>(part, lane);
+        md[0] = __shfl_sync(0xffffffffu, u, 0) * invD;
+        md[1] = __shfl_sync(0xffffffffu, u, 16) * invD;
+      }
+      // pass 2: squared deviations
+      const uint32_t z1 = runtime_zero(md[0] + md[1]);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const P nK = splat2(-K[q]), nm = splat2(-md[q]);
+        P acc[4] = {splat2(CT(0)), splat2(CT(0)), splat2(CT(0)), splat2(CT(0))};
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          if (lane + 32 * i < p.nvec) {
+            P t[NP];
+            unpack2_dep<T>(v[q][i], z1, t);
+#pragma unroll
+            for (int e = 0; e < NP; ++e) {
+              const P d = add2(SHIFT ? add2(t[e], nK) : t[e], nm);
+              acc[(i * NP + e) & 3] = fma2(d, d, acc[(i * NP + e) & 3]);
+            }
+          }
+        }
+        const P t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+        part[q] = t.x + t.y;
+      }
+      CT rs[2], mean[2], m2[2];
+      {
+        const CT u = warp_reduce_scatter<2>(part, lane);
+        m2[0] = __shfl_sync(0xffffffffu, u, 0);
+        m2[1] = __shfl_sync(0xffffffffu, u, 16);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          rs[q] = CT(1) / sqrt(m2[q] * invD + eps);
+          mean[q] = K[q] + md[q];
+        }
+      }
+      // pass 3: y for both rows from one read of (1+scale, shift)
+      const uint32_t z2 = runtime_zero(rs[0] + rs[1]);
+      const P nK0 = splat2(-K[0]), nK1 = splat2(-K[1]);
+      const P nm0 = splat2(-md[0]), nm1 = splat2(-md[1]);
+      const P rs0 = splat2(rs[0]), rs1 = splat2(rs[1]);
+      uint8_t* yr = static_cast<uint8_t*>(p.y) + row * RB;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        if (c < p.nvec) {
+          P a[NP], b[NP], t0[NP], t1[NP];
+#pragma unroll
+          for (int e = 0; e < NP; ++e) {
+            a[e] = s1[c * NP + e];
+            b[e] = sh[c * NP + e];
+          }
+          unpack2_dep<T>(v[0][i], z2, t0);
+          unpack2_dep<T>(v[1][i], z2, t1);
+#pragma unroll
+          for (int e = 0; e < NP; ++e) {
+            t0[e] = fma2(mul2(add2(SHIFT ? add2(t0[e], nK0) : t0[e], nm0), rs0), a[e], b[e]);
+            t1[e] = fma2(mul2(add2(SHIFT ? add2(t1[e], nK1) : t1[e], nm1), rs1), a[e], b[e]);
+          }
+          st_global_cs(yr + c * 16, pack2<T>(t0));
+          if (two) st_global_cs(yr + RB + c * 16, pack2<T>(t1));
+        }
+      }
+      if (lane == 0) {
+        static_cast<CT*>(p.mean)[row] = mean[0];
+        static_cast<CT*>(p.rstd)[row] = rs[0];
+        nf |= !(finite_ct(mean[0]) && finite_ct(m2[0]));
+        if (two) {
+          static_cast<CT*>(p.mean)[row + 1] = mean[1];
+          static_cast<CT*>(p.rstd)[row + 1] = rs[1];
+          nf |= !(finite_ct(mean[1]) && finite_ct(m2[1]));
+        }
+      }
+    }
+    row0 = seg_end;
+  }
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+// =====================================================================================
 // Forward, row-in-registers path for 16-bit rows (bf16 / fp16): the row stays packed in
 // registers and is consumed by mixed-precision subtracts (FHADD.{BF16,F16}: 16-bit operand,
 // fp32 result), so there is no separate expansion step.  Statistics in one pass over the
@@ -759,7 +925,7 @@ __device__ void fused_stage2(const BwdParams& p, int nc, int tid) {
 // writes dx = rstd * (g - mean(g) - xhat * mean(g*xhat)).  Packed fp32 pair math.
 // =====================================================================================
 template <typename T, int V, int R, bool FULL>
-__global__ void __launch_bounds__(384) adaln_bwd_tma(const BwdParams p) {
+__global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdParams p) {
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
   constexpr int EPV = Traits<T>::EPV;

@@ -258,6 +258,18 @@ def test_generic_path_matches_tma_path(cuda):
         assert max_rel_err(f64(a), f64(b)) <= 1e-5
 
 
+def test_auto_forward_variant_policy(cuda):
+    """variant 0 picks: two rows per warp for narrow 16-bit rows, the mixed 16-bit kernel for
+    mid widths / short ranges, the packed two-pass kernel for wide rows and 32/64-bit."""
+    def r(b, s, d, dt):
+        return nat.describe_launch(0, b, s, d, d, dt)["rows_per_stage"]
+    assert r(8, 9450, 1536, nat.AL_BF16) == 4
+    assert r(1, 32760, 3072, nat.AL_BF16) == 2
+    assert r(4, 1560, 5120, nat.AL_BF16) == 2
+    assert r(1, 32760, 5120, nat.AL_BF16) == 1
+    assert r(1, 32760, 1536, nat.AL_F32) == 1
+
+
 def test_launch_plan_for_wan14b(cuda):
     fwd = nat.describe_launch(0, 1, 32760, 5120, 5120, nat.AL_BF16)
     bwd = nat.describe_launch(1, 1, 32760, 5120, 5120, nat.AL_BF16)
@@ -528,7 +540,7 @@ def test_fused_stage2_matches_separate_kernel(cuda):
         assert torch.equal(u, v)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("dtype,shape", [(torch.bfloat16, (2, 700, 5120)),
                                          (torch.float32, (3, 257, 1536)),
                                          (torch.float16, (1, 300, 2048))])

@@ -49,6 +49,8 @@ def main():
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--which", default="fwd,bwd")
+    ap.add_argument("--variants", default="0,1,2,3,4,5,6", help="forward rows variants to time")
+    ap.add_argument("--no-ring", action="store_true", help="skip the V/R/smem ring sweep")
     args = ap.parse_args()
     dt, code, es = DT[args.dtype]
     B, S, D = args.batch, args.seq, args.dim
@@ -67,9 +69,10 @@ def main():
                           "frac": round(gbs / peak, 4), "plan": plan}), flush=True)
 
     if "fwd" in args.which:
-        cfgs = [dict(variant=v) for v in (0, 1, 2, 3, 4, 5)]
-        cfgs += [dict(V=V, R=R, smem=sm) for V, R, sm in itertools.product(
-            (1, 2, 4), (1, 2, 4), (100 * 1024, 200 * 1024))]
+        cfgs = [dict(variant=int(v)) for v in args.variants.split(",")]
+        if not args.no_ring:
+            cfgs += [dict(V=V, R=R, smem=sm) for V, R, sm in itertools.product(
+                (1, 2, 4), (1, 2, 4), (100 * 1024, 200 * 1024))]
         for c in cfgs:
             try:
                 nat.set_tuning(0, c.get("V", 0), c.get("R", 0), c.get("smem", 0), False,
@@ -83,7 +86,7 @@ def main():
     if "bwd" in args.which:
         cfgs = [dict(V=0, R=0, smem=0, variant=v) for v in (0, 2)]  # separate vs fused stage 2
         cfgs += [dict(V=V, R=R, smem=sm) for V, R, sm in itertools.product(
-            (1, 2, 4), (1, 2, 4), (100 * 1024, 150 * 1024, 200 * 1024))]
+            (1, 2, 4), (1, 2, 4), (0, 100 * 1024, 150 * 1024, 200 * 1024))]
         for c in cfgs:
             try:
                 nat.set_tuning(1, c["V"], c["R"], c["smem"], False, c.get("variant", 0))
