@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 
@@ -541,6 +542,37 @@ int check_common(int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride, in
   return AL_OK;
 }
 
+// Kernels go out with programmatic stream serialization (PDL, see ptx.cuh pdl_enter): their
+// CTAs may be scheduled while the previous kernel in the stream drains.  Which launches use it
+// is a bit mask (1 forward, 2 backward stage 1, 4 backward stage 2); AL_PDL_MASK in the
+// environment overrides the default (A/B measurements, tools/pdl_ab.sh).  Default 6: measured
+// on B200 (profiles/r1_pdl_ab.txt) the backward pair gains 1-2 % (stage 2 no longer pays a
+// full launch gap after stage 1); adding the forward (mask 7) made graph-replayed fwd+bwd
+// chains 5-10 % slower, so the forward launches plainly.
+enum { kPdlFwd = 1, kPdlBwd1 = 2, kPdlBwd2 = 4 };
+int pdl_mask() {
+  static const int m = [] {
+    const char* v = std::getenv("AL_PDL_MASK");
+    return v ? std::atoi(v) : (kPdlBwd1 | kPdlBwd2);
+  }();
+  return m;
+}
+
+cudaError_t launch_k(const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
+                     cudaStream_t st, int pdl_bit) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl_mask() & pdl_bit) ? 1 : 0;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 al::FwdParams fwd_params(const void* x, const void* scale, const void* shift, void* y,
                          void* mean, void* rstd, int64_t seq, int64_t N, int64_t dim,
                          int64_t mod_stride, int dtype, double eps, int* nonfinite,
@@ -570,8 +602,8 @@ al::FwdParams fwd_params(const void* x, const void* scale, const void* shift, vo
 
 int launch(const Plan& pl, al::FwdParams& p, void* stream, const char* what) {
   void* args[] = {&p};
-  cudaError_t e = cudaLaunchKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem,
-                                   static_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_k(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem,
+                           static_cast<cudaStream_t>(stream), kPdlFwd);
   if (e != cudaSuccess) return cuda_fail(e, what);
   return AL_OK;
 }
@@ -851,7 +883,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
     if (e != cudaSuccess) return cuda_fail(e, "backward (fused) cooperative launch");
     return AL_OK;
   }
-  e = cudaLaunchKernel(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st);
+  e = launch_k(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st, kPdlBwd1);
   if (e != cudaSuccess) return cuda_fail(e, "backward stage-1 launch");
   // stage 2: 16-byte vector form when every partial row is 16-byte aligned
   const void* rk = reduce_kernel(dtype, vec);
@@ -860,7 +892,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   const int64_t cols_per_cta = vec ? 16 * (16 / cs) : 32;
   dim3 rgrid(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
              static_cast<unsigned>(ngroups));
-  e = cudaLaunchKernel(rk, rgrid, dim3(1024), rargs, 0, st);
+  e = launch_k(rk, rgrid, dim3(1024), rargs, 0, st, kPdlBwd2);
   if (e != cudaSuccess) return cuda_fail(e, "backward stage-2 launch");
   return AL_OK;
 }

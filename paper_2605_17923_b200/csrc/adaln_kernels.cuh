@@ -141,6 +141,7 @@ struct StageWalker {
 template <typename T, int VPL, bool PACKED, bool PREFETCH = false, bool STAGED = false,
           bool RESID = false>
 __global__ void __launch_bounds__(STAGED ? 512 : 256, RESID ? 2 : 0) adaln_fwd_rows(const FwdParams p) {
+  pdl_enter();
   static_assert(!(RESID && STAGED), "the gated residual is not staged");
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
@@ -380,6 +381,7 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256, RESID ? 2 : 0) adaln_fwd_r
 // =====================================================================================
 template <typename T, int VPL>
 __global__ void __launch_bounds__(256) adaln_fwd_rows2(const FwdParams p) {
+  pdl_enter();
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
   constexpr int EPV = Traits<T>::EPV;
@@ -548,6 +550,7 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows2(const FwdParams p) {
 // =====================================================================================
 template <typename T, int VPL>
 __global__ void __launch_bounds__(256) adaln_fwd_rows16(const FwdParams p) {
+  pdl_enter();
   static_assert(sizeof(T) == 2, "16-bit rows only");
   using P = float2;
   constexpr int NP = 4;  // pairs per 16-byte vector
@@ -652,6 +655,7 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows16(const FwdParams p) {
 // =====================================================================================
 template <typename T, int V, int R>
 __global__ void __launch_bounds__(512) adaln_fwd_wide(const FwdParams p) {
+  pdl_enter();
   using CT = typename Traits<T>::CT;
   constexpr int EPV = Traits<T>::EPV;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -926,6 +930,7 @@ __device__ void fused_stage2(const BwdParams& p, int nc, int tid) {
 // =====================================================================================
 template <typename T, int V, int R, bool FULL>
 __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdParams p) {
+  pdl_enter();
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
   constexpr int EPV = Traits<T>::EPV;
@@ -1191,6 +1196,7 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce_vec(const CT* __restric
                                                              CT* __restrict__ dshift, int64_t N,
                                                              int64_t S_grp, int64_t D, int64_t G,
                                                              int64_t nslots) {
+  pdl_enter();
   constexpr int VE = 16 / sizeof(CT);  // columns per 16-byte vector
   constexpr int COLS = 16 * VE;        // columns per CTA
   __shared__ double part[2][32][COLS + 1];
@@ -1268,6 +1274,7 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce(const CT* __restrict__ 
                                                          CT* __restrict__ dshift, int64_t N,
                                                          int64_t S_grp, int64_t D, int64_t G,
                                                          int64_t nslots) {
+  pdl_enter();
   __shared__ double part[2][32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t g = blockIdx.y;
@@ -1301,6 +1308,7 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce(const CT* __restrict__ 
 // =====================================================================================
 template <typename T>
 __global__ void __launch_bounds__(256) adaln_fwd_generic(const FwdParams p) {
+  pdl_enter();
   using CT = typename Traits<T>::CT;
   const int lane = threadIdx.x & 31;
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1343,6 +1351,7 @@ __global__ void __launch_bounds__(256) adaln_fwd_generic(const FwdParams p) {
 // normalises x_out.
 template <typename T>
 __global__ void __launch_bounds__(256) gate_residual_generic(const FwdParams p) {
+  pdl_enter();
   using CT = typename Traits<T>::CT;
   const T* x = static_cast<const T*>(p.x);
   const T* f = static_cast<const T*>(p.f);
@@ -1363,6 +1372,7 @@ __global__ void __launch_bounds__(256) gate_residual_generic(const FwdParams p) 
 
 template <typename T>
 __global__ void __launch_bounds__(256) adaln_bwd_generic(const BwdParams p) {
+  pdl_enter();
   using CT = typename Traits<T>::CT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int64_t k = blockIdx.x;

@@ -92,6 +92,19 @@ __device__ __forceinline__ uint4 ld_shared_v4(const void* p) {
   return v;
 }
 
+// Programmatic dependent launch (PDL).  The C ABI launches every kernel with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs may be scheduled while
+// the previous kernel in the stream drains (hiding launch latency -- it matters at short
+// sequences, where a kernel runs only ~10 us).  griddepcontrol.wait blocks until that previous
+// kernel has completed and its writes are visible, so it comes before any dependent load;
+// launch_dependents lets the next PDL kernel be scheduled as soon as SM resources free up (it
+// still waits for this kernel's completion before touching memory).  Without the launch
+// attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // 32-bit shared-window address form: no generic->shared conversion per access.
 __device__ __forceinline__ uint4 ld_shared_v4_u32(uint32_t a) {
   uint4 v;
