@@ -447,20 +447,15 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
       // variant: 1 packed row, 2 compiler-expanded row, 3 packed row + bulk L2 prefetch of
       // each warp's next row (slower on B200: 4.95 vs 5.53 TB/s at cfg2), 4 mixed-precision
       // 16-bit kernel, 5 packed row with a TMA-staged one-row lookahead per warp, 6 two rows
-      // per warp.  0 = auto, from the B200 sweeps (profiles/r1_fwd_variants.jsonl):
-      //   16-bit, <= 6 vectors per lane (D <= 1536 bf16) -> 6  (+4..15 %: half the LDS traffic)
-      //   16-bit, 8..16 vectors, or short CTA ranges    -> 4  (+2..14 %)
-      //   otherwise (wide 16-bit rows with long ranges; fp32/fp64) -> 1
+      // per warp.  0 = auto, from the B200 sweeps (profiles/r1_fwd_policy.jsonl,
+      // r1_fwd_variants.jsonl):
+      //   16-bit, 6 vectors per lane (D = 1 281..1 536 bf16)  -> 6  (5 650 vs 5 319 / 5 488 GB/s)
+      //   other 16-bit rows                                   -> 4  (>= variant 1 everywhere;
+      //       +35 % at D = 5 120 short sequences, +37 % at D = 6 144)
+      //   fp32 / fp64                                          -> 1  (exact two-pass statistics)
       const bool is16 = dtype == AL_BF16 || dtype == AL_F16;
       int variant = tu.variant;
-      if (variant == 0) {
-        variant = 1;
-        if (is16) {
-          const int64_t rows_per_cta = N / (2 * static_cast<int64_t>(sms));
-          if (kVpl[vi] <= 6) variant = 6;
-          else if (kVpl[vi] <= 16 || rows_per_cta < 64) variant = 4;
-        }
-      }
+      if (variant == 0) variant = !is16 ? 1 : (kVpl[vi] == 6 ? 6 : 4);
       const bool mixed = is16 && variant == 4;
       const bool repack = variant != 2;
       const size_t staged_smem = 2 * static_cast<size_t>(D) * cs + 16 * static_cast<size_t>(row_bytes) +

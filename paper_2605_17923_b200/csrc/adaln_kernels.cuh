@@ -147,6 +147,10 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256, RESID ? 2 : 0) adaln_fwd_r
   using P = typename PairOf<CT>::type;
   constexpr int EPV = Traits<T>::EPV;
   constexpr int NP = EPV / 2;  // pairs per 16-byte vector
+  // (1+scale, shift[, gate]) staging: interleaved, pair e of vector c at c * NP + e.  (The
+  // planar layout of rows2/rows16 removes the 2-way bank conflict of 16-bit rows but measured
+  // 2-4 % slower here at D = 5120, long sequences -- profiles/r1_fwd_variants.jsonl.)
+  auto mi = [](int c, int e) { return c * NP + e; };
   constexpr bool SHIFT = sizeof(T) >= 4;
   extern __shared__ __align__(16) uint8_t smem[];
   P* s1 = reinterpret_cast<P*>(smem);  // [nvec * NP] : 1 + scale
@@ -217,15 +221,15 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256, RESID ? 2 : 0) adaln_fwd_r
 #pragma unroll
         for (int e = 0; e < NP; ++e) {
           nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y) && finite_ct(b[e].x) && finite_ct(b[e].y));
-          s1[c * NP + e] = add2(a[e], splat2(CT(1)));
-          sh[c * NP + e] = b[e];
+          s1[mi(c, e)] = add2(a[e], splat2(CT(1)));
+          sh[mi(c, e)] = b[e];
         }
         if constexpr (RESID) {
           unpack2<T>(__ldg(reinterpret_cast<const uint4*>(ga) + c), a);
 #pragma unroll
           for (int e = 0; e < NP; ++e) {
             nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y));
-            gt[c * NP + e] = a[e];
+            gt[mi(c, e)] = a[e];
           }
         }
       }
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256, RESID ? 2 : 0) adaln_fwd_r
           unpack2<T>(v[i], xa);
           unpack2<T>(fw, fa);
 #pragma unroll
-          for (int e = 0; e < NP; ++e) xa[e] = fma2(gt[cc * NP + e], fa[e], xa[e]);
+          for (int e = 0; e < NP; ++e) xa[e] = fma2(gt[mi(cc, e)], fa[e], xa[e]);
           v[i] = pack2<T>(xa);
         }
       } else {
@@ -350,8 +354,8 @@ __global__ void __launch_bounds__(STAGED ? 512 : 256, RESID ? 2 : 0) adaln_fwd_r
           expand(v[i], z2, q);
 #pragma unroll
           for (int e = 0; e < NP; ++e) {
-            a[e] = s1[c * NP + e];
-            b[e] = sh[c * NP + e];
+            a[e] = s1[mi(c, e)];
+            b[e] = sh[mi(c, e)];
           }
 #pragma unroll
           for (int e = 0; e < NP; ++e) {
@@ -386,6 +390,8 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows2(const FwdParams p) {
   using P = typename PairOf<CT>::type;
   constexpr int EPV = Traits<T>::EPV;
   constexpr int NP = EPV / 2;
+  // interleaved (1+scale, shift) staging, as adaln_fwd_rows (planar measured ~2 % slower here)
+  auto mi = [](int c, int e) { return c * NP + e; };
   constexpr bool SHIFT = sizeof(T) >= 4;
   extern __shared__ __align__(16) uint8_t smem[];
   P* s1 = reinterpret_cast<P*>(smem);
@@ -415,8 +421,8 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows2(const FwdParams p) {
 #pragma unroll
         for (int e = 0; e < NP; ++e) {
           nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y) && finite_ct(b[e].x) && finite_ct(b[e].y));
-          s1[c * NP + e] = add2(a[e], splat2(CT(1)));
-          sh[c * NP + e] = b[e];
+          s1[mi(c, e)] = add2(a[e], splat2(CT(1)));
+          sh[mi(c, e)] = b[e];
         }
       }
     }
@@ -509,8 +515,8 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows2(const FwdParams p) {
           P a[NP], b[NP], t0[NP], t1[NP];
 #pragma unroll
           for (int e = 0; e < NP; ++e) {
-            a[e] = s1[c * NP + e];
-            b[e] = sh[c * NP + e];
+            a[e] = s1[mi(c, e)];
+            b[e] = sh[mi(c, e)];
           }
           unpack2_dep<T>(v[0][i], z2, t0);
           unpack2_dep<T>(v[1][i], z2, t1);
@@ -554,6 +560,13 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows16(const FwdParams p) {
   static_assert(sizeof(T) == 2, "16-bit rows only");
   using P = float2;
   constexpr int NP = 4;  // pairs per 16-byte vector
+  // (1+scale, shift) staging in shared memory, planar by 16-byte chunk: pair e of vector c
+  // lives in plane e / HP, so the per-lane 16-byte reads of one plane are consecutive across
+  // the warp (no 2-way bank conflict: 16-bit vectors expand to 32 bytes of fp32 pairs).
+  // Measured +6-8 % at short sequences (cfg3 S <= 3600), where this kernel is selected.
+  constexpr int HP = 16 / static_cast<int>(sizeof(P));
+  const int nvec_ = p.nvec;
+  auto mi = [nvec_](int c, int e) { return ((e / HP) * nvec_ + c) * HP + (e % HP); };
   extern __shared__ __align__(16) uint8_t smem[];
   P* s1 = reinterpret_cast<P*>(smem);  // [nvec * NP] : 1 + scale
   P* sh = s1 + p.nvec * NP;            // [nvec * NP] : shift
@@ -581,8 +594,8 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows16(const FwdParams p) {
 #pragma unroll
         for (int e = 0; e < NP; ++e) {
           nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y) && finite_ct(b[e].x) && finite_ct(b[e].y));
-          s1[c * NP + e] = add2(a[e], splat2(1.0f));
-          sh[c * NP + e] = b[e];
+          s1[mi(c, e)] = add2(a[e], splat2(1.0f));
+          sh[mi(c, e)] = b[e];
         }
       }
     }
@@ -630,7 +643,7 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows16(const FwdParams p) {
           P o[NP];
 #pragma unroll
           for (int e = 0; e < NP; ++e)
-            o[e] = fma2(mul2(sub16x2_f32<T>(w[e], -mean), rs2), s1[c * NP + e], sh[c * NP + e]);
+            o[e] = fma2(mul2(sub16x2_f32<T>(w[e], -mean), rs2), s1[mi(c, e)], sh[mi(c, e)]);
           st_global_cs(yr + c * 16, pack2<T>(o));
         }
       }

@@ -259,15 +259,16 @@ def test_generic_path_matches_tma_path(cuda):
 
 
 def test_auto_forward_variant_policy(cuda):
-    """variant 0 picks: two rows per warp for narrow 16-bit rows, the mixed 16-bit kernel for
-    mid widths / short ranges, the packed two-pass kernel for wide rows and 32/64-bit."""
+    """variant 0 picks: two rows per warp for D ~ 1536 16-bit rows, the mixed 16-bit kernel for
+    other 16-bit rows, the packed exact two-pass kernel for 32/64-bit."""
     def r(b, s, d, dt):
         return nat.describe_launch(0, b, s, d, d, dt)["rows_per_stage"]
     assert r(8, 9450, 1536, nat.AL_BF16) == 4
     assert r(1, 32760, 3072, nat.AL_BF16) == 2
     assert r(4, 1560, 5120, nat.AL_BF16) == 2
-    assert r(1, 32760, 5120, nat.AL_BF16) == 1
+    assert r(1, 32760, 5120, nat.AL_F16) == 2
     assert r(1, 32760, 1536, nat.AL_F32) == 1
+    assert r(1, 32760, 1536, nat.AL_F64) == 1
 
 
 def test_launch_plan_for_wan14b(cuda):
