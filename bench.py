@@ -316,8 +316,11 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize(dev)
     barrier(world)
     t0 = time.perf_counter()
+    step_s = []
     for _ in range(e2e_steps):
-        out, gr = e2e_step()
+        ts = time.perf_counter()
+        out, gr = e2e_step()  # returns after the D2H of its results completed
+        step_s.append(time.perf_counter() - ts)
     torch.cuda.synchronize(dev)
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, world)
     barrier(world)
@@ -388,6 +391,7 @@ def run_ours(args, world, rank, local):
                             "avg_ms": round(bwd_avg, 5), "bytes": nb["bwd"], "plan": bplan}},
         "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                "step_ms_min_max": [round(1e3 * min(step_s), 2), round(1e3 * max(step_s), 2)],
                 "path": "adaln_forward + adaln_backward_naive on pinned torch CPU bf16 tensors"},
         "cpu_baseline": cpu,
         "gpu_launches": 3 * K,
@@ -408,7 +412,7 @@ def main():
     ap.add_argument("--workload", choices=["adaln", "dit"], default="adaln")
     ap.add_argument("--seq", type=int, default=32760)
     ap.add_argument("--dim", type=int, default=5120)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-rows", type=int, default=8192)
     ap.add_argument("--ref-rows", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
