@@ -79,6 +79,7 @@ struct Table {
   FwdFn rows[kNumVpl];
   FwdFn rows_rp[kNumVpl];  // PACKED variant (row kept packed, re-expanded per pass)
   FwdFn wide[3][3];  // [V idx][R idx], V in {1,2,4}, R in {1,2,4}
+  FwdFn ring[3][3];  // backward-style TMA-ring forward (variant 7)
   BwdFn bwd[3][3];
   BwdFn bwd_full[3][3];  // nvec == V * consumers: ownership predicates compiled out
   FwdFn fwd_generic;
@@ -113,6 +114,15 @@ struct Table {
     wide[2][0] = al::adaln_fwd_wide<T, 4, 1>;
     wide[2][1] = al::adaln_fwd_wide<T, 4, 2>;
     wide[2][2] = al::adaln_fwd_wide<T, 4, 4>;
+    ring[0][0] = al::adaln_fwd_ring<T, 1, 1>;
+    ring[0][1] = al::adaln_fwd_ring<T, 1, 2>;
+    ring[0][2] = al::adaln_fwd_ring<T, 1, 4>;
+    ring[1][0] = al::adaln_fwd_ring<T, 2, 1>;
+    ring[1][1] = al::adaln_fwd_ring<T, 2, 2>;
+    ring[1][2] = al::adaln_fwd_ring<T, 2, 4>;
+    ring[2][0] = al::adaln_fwd_ring<T, 4, 1>;
+    ring[2][1] = al::adaln_fwd_ring<T, 4, 2>;
+    ring[2][2] = al::adaln_fwd_ring<T, 4, 4>;
     bwd[0][0] = al::adaln_bwd_tma<T, 1, 1, false>;
     bwd_full[0][0] = al::adaln_bwd_tma<T, 1, 1, true>;
     bwd[0][1] = al::adaln_bwd_tma<T, 1, 2, false>;
@@ -165,11 +175,11 @@ auto with_table(int dtype, F&& f) {
 }
 
 // path: 1 = TMA ring (wide forward / backward), 2 = rows-in-registers forward
-const void* tma_kernel(int kernel, int dtype, int V, int R, bool full = false) {
+const void* tma_kernel(int kernel, int dtype, int V, int R, bool full = false, bool ring = false) {
   const int a = vidx(V), b = vidx(R);
   return with_table(dtype, [&](const auto& t) {
     if (kernel) return full ? (const void*)t.bwd_full[a][b] : (const void*)t.bwd[a][b];
-    return (const void*)t.wide[a][b];
+    return ring ? (const void*)t.ring[a][b] : (const void*)t.wide[a][b];
   });
 }
 const void* rows_kernel(int dtype, int vi, bool repack) {
@@ -354,11 +364,12 @@ int occupancy(const Plan& pl, int dev, int* occ) {
 constexpr int kRingPerSm = 200 * 1024;
 
 bool ring_plan(int kernel, int dtype, int64_t nvec, int row_bytes, int cs, const Tuning& tu,
-               int dev, Plan* pl) {
+               int dev, Plan* pl, bool fwd_ring = false) {
   int V = tu.V;
-  // __launch_bounds__ of the kernels: backward V=1 takes up to 21 consumer warps (<= 93 regs)
-  const int max_threads = kernel ? (V == 1 ? 704 : 384) : 512;
-  const int vcap = kernel ? 352 : 256;
+  // __launch_bounds__ of the kernels: backward V=1 takes up to 21 consumer warps (<= 93 regs);
+  // the ring forward is bounded at 384 like the backward
+  const int max_threads = kernel ? (V == 1 ? 704 : 384) : (fwd_ring ? 384 : 512);
+  const int vcap = (kernel || fwd_ring) ? 352 : 256;
   if (V == 0) {
     if (kernel == 1) {
       // backward: 2 vectors (16 columns) per thread amortise the per-row reductions best
@@ -380,7 +391,7 @@ bool ring_plan(int kernel, int dtype, int64_t nvec, int row_bytes, int cs, const
   const bool full = kernel == 1 && nvec == static_cast<int64_t>(V) * nc;
   while (true) {
     const int64_t stage = static_cast<int64_t>(tensors) * R * row_bytes;
-    const void* fn = tma_kernel(kernel, dtype, V, R, full);
+    const void* fn = tma_kernel(kernel, dtype, V, R, full, fwd_ring);
     int budget = tu.smem_budget;
     if (budget == 0) {
       int k_reg = 1;
@@ -436,7 +447,28 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
   if (vec_ok) {
     const int64_t nvec = D / epv;
     const int row_bytes = static_cast<int>(D * es);
-    if (kernel == 0 && tu.V == 0 && tu.R == 0 && nvec <= 32 * kMaxVpl) {
+    // Forward TMA-ring kernel (variant 7).  Auto-selected (profiles/r1_fwd_ring.jsonl) for
+    // fp32 rows of >= 768 vectors (D >= 3 072: 5 353-5 711 vs 4 016-5 184 GB/s for the rows
+    // kernel, two-pass statistics) and for any row too wide for the rows kernels (bf16
+    // D = 8 192: 5 485 vs 2 141 GB/s for the old wide kernel); 4 vectors per thread, 2 (16-bit)
+    // or 4 (32/64-bit) rows per stage, ~100 KB ring per CTA (2 CTAs per SM).
+    bool fwd_ring = false;
+    if (kernel == 0) {
+      const bool auto_cfg = tu.variant == 0 && tu.V == 0 && tu.R == 0;
+      if (tu.variant == 7) {
+        fwd_ring = ring_plan(kernel, dtype, nvec, row_bytes, cs, tu, dev, &pl, true);
+      } else if (auto_cfg && !tu.force_generic &&
+                 ((dtype == AL_F32 && nvec >= 32 * kMaxVpl) || nvec > 32 * kMaxVpl)) {
+        Tuning rt = tu;
+        rt.V = 4;
+        rt.R = (dtype == AL_F32 || dtype == AL_F64) ? 4 : 2;
+        rt.smem_budget = 100 * 1024;
+        fwd_ring = ring_plan(kernel, dtype, nvec, row_bytes, cs, rt, dev, &pl, true);
+      }
+    }
+    if (fwd_ring || (kernel == 0 && tu.variant == 7)) {
+      // planned above (a failed variant-7 plan leaves pl.path == 0: generic)
+    } else if (kernel == 0 && tu.V == 0 && tu.R == 0 && nvec <= 32 * kMaxVpl) {
       // rows-in-registers forward
       int vi = 0;
       while (32 * kVpl[vi] < nvec) ++vi;
@@ -640,6 +672,10 @@ int al_device_init(int device) {
           for (bool full : {false, true}) {
             rc = ensure_attr(tma_kernel(kernel, dt, V, R, full), device);
             if (rc) return rc;
+            if (kernel == 0) {
+              rc = ensure_attr(tma_kernel(kernel, dt, V, R, full, true), device);
+              if (rc) return rc;
+            }
           }
       if (kernel == 0)
         for (int vi = 0; vi < kNumVpl; ++vi) {
@@ -730,14 +766,17 @@ int al_adaln_gate_residual_forward(const void* x, const void* f, const void* gat
     return fail(AL_ERR_SHAPE, "null tensor pointer");
   if (x_out == x || x_out == f) return fail(AL_ERR_VALUE, "x_out may not alias x or f");
   const void* vp[7] = {x, f, gate, x_out, y, scale, shift};
-  Plan pl;
-  rc = make_plan(0, N, dim, mod_stride, dtype, 0, vp, 7, &pl);
-  if (rc) return rc;
-  if (pl.path == 2) {
-    // fused: swap the rows kernel for its gated-residual twin (same geometry, +1 smem row)
+  const int es = elem_size(dtype);
+  bool vec_ok = (dim * es) % 16 == 0 && (mod_stride * es) % 16 == 0;
+  for (int i = 0; i < 7 && vec_ok; ++i) vec_ok = aligned16(vp[i]);
+  const int64_t nvec = dim * es / 16;
+  if (vec_ok && nvec <= 32 * kMaxVpl) {
+    // fused: the rows kernel's gated-residual twin (one warp per row, +1 smem row for gate)
     int vi = 0;
-    while (kVpl[vi] < pl.V) ++vi;
-    Plan pr = pl;
+    while (32 * kVpl[vi] < nvec) ++vi;
+    Plan pr;
+    pr.path = 2;
+    pr.V = kVpl[vi];
     pr.fn = resid_kernel(dtype, vi);
     pr.threads = 256;
     pr.smem = 3 * static_cast<size_t>(dim) * ct_size(dtype);

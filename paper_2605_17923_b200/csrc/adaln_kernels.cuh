@@ -865,6 +865,255 @@ __global__ void __launch_bounds__(512) adaln_fwd_wide(const FwdParams p) {
 }
 
 // =====================================================================================
+// Forward, TMA ring in the backward's mould (variant 7; the default for 32-bit rows of
+// D >= 2048 and for 16-bit rows wider than the rows kernels take).
+// One producer lane streams R rows of x per stage into an NS-deep shared-memory ring with 1-D
+// bulk copies; consumer thread t owns 16-byte column vectors t + j*nc.  Per stage: the owned
+// vectors of the R rows are read once from shared memory and kept PACKED in registers, the row
+// sums are reduce-scattered within the warp and combined across warps through a named barrier,
+// the slot is released, and y = (x - mean) * rstd * (1 + scale) + shift is written from the
+// registers.  Packed fp32 pair math; (1 + scale, shift) of the owned columns live in registers.
+// Statistics of d = x - K (K = the row's first element):
+//   16-bit rows: one pass of sum d and sum d^2 (d exact in fp32; the cancellation error
+//     ~2^-24 sqrt(D) (1 + (K - mean)^2 / var) is far below the 2^-9 output rounding);
+//   32/64-bit rows: exact two passes from the registers (sum d, barrier, sum (d - mean_d)^2,
+//     barrier) -- a single pass can exceed 1e-5 relative on rows whose first element is a
+//     far outlier.
+// =====================================================================================
+template <typename T, int V, int R>
+__global__ void __launch_bounds__(384) adaln_fwd_ring(const FwdParams p) {
+  pdl_enter();
+  using CT = typename Traits<T>::CT;
+  using P = typename PairOf<CT>::type;
+  constexpr int NP = Traits<T>::EPV / 2;
+  constexpr bool TWO = sizeof(T) >= 4;
+  constexpr int NV = TWO ? R : 2 * R;  // row sums reduced per barrier
+  extern __shared__ __align__(128) uint8_t smem[];
+
+  const int nc = blockDim.x - 32;
+  const int ncw = nc >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NS = p.nstages;
+  const int RB = p.row_bytes;
+  const int stage_bytes = R * RB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(NS) * stage_bytes);
+  uint64_t* empty = full + NS;
+  // [2 parities][ncw][2R]: (sum d, sum d^2) per row; two-pass rows use the halves for the
+  // two passes
+  CT* red = reinterpret_cast<CT*>(empty + NS);
+
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ncw);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == ncw) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const uint8_t* xb = static_cast<const uint8_t*>(p.x);
+      StageWalker w;
+      w.init(r0, r1, p.S_grp);
+      int s = 0;
+      uint32_t f = 0;
+      while (!w.done()) {
+        int64_t start, g;
+        const int rows = w.next(R, start, g);
+        if (f > 0) mbar_wait(&empty[s], (f - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows * RB));
+        uint8_t* dst = smem + static_cast<size_t>(s) * stage_bytes;
+        for (int rr = 0; rr < rows; ++rr)
+          bulk_g2s(dst + rr * RB, xb + (start + rr) * RB, RB, &full[s], pol);
+        if (++s == NS) {
+          s = 0;
+          ++f;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  uint32_t vmask = 0u;
+  int coff[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    coff[j] = (tid + j * nc) * 16;
+    if (tid + j * nc < p.nvec) vmask |= 1u << j;
+  }
+  const CT invD = CT(1) / static_cast<CT>(p.D);
+  const CT eps = static_cast<CT>(p.eps);
+  const uint32_t ring_u = smem_addr(smem);
+  bool nf = false;
+
+  // warp reduce-scatter of NV row sums, then the cross-warp totals spread over the lanes
+  auto reduce_rows = [&](const CT* v, CT* buf, CT* out) {
+    constexpr int GRP = 32 / NV;
+    const CT u = warp_reduce_scatter<NV>(v, lane);
+    if ((lane & (GRP - 1)) == 0) buf[warp * NV + lane / GRP] = u;
+    named_bar_sync(1, nc);
+    return [=](CT* o) {
+      const int nval = ncw * NV;
+      CT s_l = CT(0);
+      for (int i = lane; i < nval; i += 32) s_l += buf[i];
+#pragma unroll
+      for (int off = NV; off < 32; off <<= 1) s_l += __shfl_xor_sync(0xffffffffu, s_l, off);
+#pragma unroll
+      for (int q = 0; q < NV; ++q) o[q] = __shfl_sync(0xffffffffu, s_l, q);
+    };
+  };
+
+  P s1[V][NP], shv[V][NP];
+  int64_t cur_g = -1;
+  StageWalker w;
+  w.init(r0, r1, p.S_grp);
+  int s = 0;
+  uint32_t ph = 0;
+  int it = 0;
+  while (!w.done()) {
+    int64_t rb, g;
+    const int rows = w.next(R, rb, g);
+    if (g != cur_g) {
+      cur_g = g;
+      const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
+      const uint8_t* sf = static_cast<const uint8_t*>(p.shift) + g * p.mod_stride * sizeof(T);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const bool ok = vmask >> j & 1;
+        unpack2<T>(ok ? __ldg(reinterpret_cast<const uint4*>(sc + coff[j])) : make_uint4(0, 0, 0, 0), s1[j]);
+        unpack2<T>(ok ? __ldg(reinterpret_cast<const uint4*>(sf + coff[j])) : make_uint4(0, 0, 0, 0), shv[j]);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          nf |= !(finite_ct(s1[j][e].x) && finite_ct(s1[j][e].y) && finite_ct(shv[j][e].x) &&
+                  finite_ct(shv[j][e].y));
+          s1[j][e] = add2(s1[j][e], splat2(CT(1)));
+        }
+      }
+    }
+    mbar_wait(&full[s], ph);
+    const uint32_t st = ring_u + static_cast<uint32_t>(s * stage_bytes);
+    CT* rd = red + (it & 1) * (ncw * 2 * R);
+
+    // phase 1: first-pass sums from the packed row slice, kept in registers
+    uint4 xr[R][V];
+    CT K[R], rowsum[2 * R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const bool live = rr < rows;
+      {
+        P k0[NP];
+        unpack2<T>(live ? ld_shared_v4_u32(st + rr * RB) : make_uint4(0, 0, 0, 0), k0);
+        K[rr] = k0[0].x;
+      }
+      const P nK = splat2(-K[rr]);
+      P a1[2] = {splat2(CT(0)), splat2(CT(0))}, a2[2] = {splat2(CT(0)), splat2(CT(0))};
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const bool ok = live && (vmask >> j & 1);
+        xr[rr][j] = ok ? ld_shared_v4_u32(st + static_cast<uint32_t>(rr * RB + coff[j]))
+                       : make_uint4(0, 0, 0, 0);
+        if (ok) {
+          P q[NP];
+          unpack2<T>(xr[rr][j], q);
+#pragma unroll
+          for (int e = 0; e < NP; ++e) {
+            const P d = add2(q[e], nK);
+            a1[e & 1] = add2(a1[e & 1], d);
+            if constexpr (!TWO) a2[e & 1] = fma2(d, d, a2[e & 1]);
+          }
+        }
+      }
+      const P t1 = add2(a1[0], a1[1]), t2 = add2(a2[0], a2[1]);
+      if constexpr (TWO) {
+        rowsum[rr] = t1.x + t1.y;
+      } else {
+        rowsum[2 * rr] = t1.x + t1.y;
+        rowsum[2 * rr + 1] = t2.x + t2.y;
+      }
+    }
+    auto fin1 = reduce_rows(rowsum, rd, nullptr);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // the stage is in registers: hand the slot back
+
+    CT md[R], m2v[R];
+    {
+      CT tot[2 * R];
+      fin1(tot);
+      if constexpr (TWO) {
+        // second pass: centred squares from the registers
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          md[rr] = tot[rr] * invD;
+          const P nK = splat2(-K[rr]), nmd = splat2(-md[rr]);
+          P a2[2] = {splat2(CT(0)), splat2(CT(0))};
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            if (rr < rows && (vmask >> j & 1)) {
+              P q[NP];
+              unpack2<T>(xr[rr][j], q);
+#pragma unroll
+              for (int e = 0; e < NP; ++e) {
+                const P d = add2(add2(q[e], nK), nmd);
+                a2[e & 1] = fma2(d, d, a2[e & 1]);
+              }
+            }
+          }
+          const P t2 = add2(a2[0], a2[1]);
+          rowsum[rr] = t2.x + t2.y;
+        }
+        auto fin2 = reduce_rows(rowsum, rd + ncw * R, nullptr);
+        fin2(m2v);
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          md[rr] = tot[2 * rr] * invD;
+          m2v[rr] = fmax(tot[2 * rr + 1] - tot[2 * rr] * md[rr], CT(0));
+        }
+      }
+    }
+
+    // phase 2: y = ((x - K) - mean_d) * rstd * (1 + scale) + shift
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (rr < rows) {
+        const int64_t row = rb + rr;
+        const CT rs = CT(1) / sqrt(m2v[rr] * invD + eps);
+        const P nK = splat2(-K[rr]), nmd = splat2(-md[rr]), rs2 = splat2(rs);
+        uint8_t* yrow = static_cast<uint8_t*>(p.y) + row * RB;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if (vmask >> j & 1) {
+            P q[NP];
+            unpack2<T>(xr[rr][j], q);
+#pragma unroll
+            for (int e = 0; e < NP; ++e)
+              q[e] = fma2(mul2(add2(add2(q[e], nK), nmd), rs2), s1[j][e], shv[j][e]);
+            st_global_cs(yrow + coff[j], pack2<T>(q));
+          }
+        }
+        if (tid == 0) {
+          static_cast<CT*>(p.mean)[row] = K[rr] + md[rr];
+          static_cast<CT*>(p.rstd)[row] = rs;
+          nf |= !(finite_ct(md[rr]) && finite_ct(m2v[rr]));
+        }
+      }
+    }
+    if (++s == NS) {
+      s = 0;
+      ph ^= 1;
+    }
+    ++it;
+  }
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+// =====================================================================================
 // Fused stage 2 (cooperative launch only: every CTA of the grid is co-resident).
 // After its stage-1 partials are stored, each CTA passes a grid barrier (one atomic per CTA
 // on a host-zeroed counter), then reduces a contiguous share of the (group, 16-byte column

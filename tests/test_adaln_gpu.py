@@ -269,6 +269,13 @@ def test_auto_forward_variant_policy(cuda):
     assert r(1, 32760, 5120, nat.AL_F16) == 2
     assert r(1, 32760, 1536, nat.AL_F32) == 1
     assert r(1, 32760, 1536, nat.AL_F64) == 1
+    # the TMA-ring forward: fp32 rows of >= 768 vectors, and rows too wide for the rows kernels
+    for b, s, d, dt, rows_per_stage in ((1, 32760, 3072, nat.AL_F32, 4), (1, 32760, 5120, nat.AL_F32, 4),
+                                        (1, 32760, 8192, nat.AL_BF16, 2)):
+        info = nat.describe_launch(0, b, s, d, d, dt)
+        assert info["path"] == "tma" and info["vecs_per_thread"] == 4
+        assert info["rows_per_stage"] == rows_per_stage
+    assert nat.describe_launch(0, 1, 32760, 2048, 2048, nat.AL_F32)["path"] == "rows"
 
 
 def test_launch_plan_for_wan14b(cuda):
@@ -541,7 +548,7 @@ def test_fused_stage2_matches_separate_kernel(cuda):
         assert torch.equal(u, v)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("dtype,shape", [(torch.bfloat16, (2, 700, 5120)),
                                          (torch.float32, (3, 257, 1536)),
                                          (torch.float16, (1, 300, 2048))])
@@ -585,3 +592,29 @@ def test_host_pipeline_matches_device_path(shape, mod, cuda):
     x_bad.view(-1)[12345] = float("nan")
     with pytest.raises(NonFiniteInput):
         adaln_forward(x_bad, sc, sh)
+
+
+@pytest.mark.parametrize("dtype,shape", [(torch.float32, (2, 300, 4096)), (torch.float32, (1, 257, 5120)),
+                                         (torch.bfloat16, (2, 300, 8192)), (torch.float64, (1, 65, 2048)),
+                                         (torch.bfloat16, (3, 50, 5000))])
+def test_ring_forward_vs_oracle(dtype, shape, cuda):
+    """Variant 7 (TMA-ring forward): 32/64-bit rows use exact two passes, so an offset row whose
+    first element is a 12-sigma outlier still meets the fp32 bar; 16-bit rows one shifted pass."""
+    b, s, d = shape
+    x, sc, sh, _ = make(b, s, d, dtype, cuda, seed=d + s, offset=50.0)
+    x[:, ::7, 0] += 12.0  # outlier first elements (the shift K of those rows)
+    yo, muo, rso = oracle.forward_batched(f64(x), f64(sc), f64(sh), 1e-6, threads=0)
+    try:
+        nat.set_tuning(0, variant=7)
+        plan = nat.describe_launch(0, b, s, d, d, nat.AL_F32 if dtype == torch.float32 else
+                                   (nat.AL_BF16 if dtype == torch.bfloat16 else nat.AL_F64))
+        y, mu, rs = fused_forward(x, sc, sh)
+        y2, _, _ = fused_forward(x, sc, sh)
+    finally:
+        nat.set_tuning(0)
+    if d % 8 == 0:
+        assert plan["path"] == "tma"
+    tol = {torch.float32: 1e-5, torch.bfloat16: 2e-2, torch.float64: 1e-11}[dtype]
+    assert max_rel_err(f64(y), yo) <= tol
+    assert max_rel_err(f64(rs), rso) <= (1e-5 if dtype != torch.float64 else 1e-11)
+    assert torch.equal(y, y2)

@@ -68,12 +68,14 @@ def test_matches_oracle(dtype, shape, cuda):
 @pytest.mark.parametrize("shape", [(2, 300, 1536), (1, 200, 5120), (2, 9, 12288)])
 def test_y_equals_forward_of_x_out_bitwise(dtype, shape, cuda):
     """The fused kernel's y/mean/rstd are exactly the one-row-per-warp forward (variant 1)
-    applied to its x_out."""
+    applied to its x_out; rows too wide for it take the unfused composition (residual kernel,
+    then the default forward)."""
     b, s, d = shape
     x, f, gate, sc, sh = make(b, s, d, dtype, cuda, seed=7)
     xo, y, mu, rs = fused_gate_residual_forward(x, f, gate, sc, sh)
+    rows_kernel = d * x.element_size() // 16 <= 32 * 24
     try:
-        nat.set_tuning(0, variant=1)
+        nat.set_tuning(0, variant=1 if rows_kernel else 0)
         y2, mu2, rs2 = fused_forward(xo, sc, sh)
     finally:
         nat.set_tuning(0)

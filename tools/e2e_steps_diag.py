@@ -28,12 +28,19 @@ dyh = torch.randn(1, S, D).to(torch.bfloat16).pin_memory()
 sc = (0.1 * torch.randn(1, D)).to(torch.bfloat16).pin_memory()
 total = 5 * xh.numel() * 2 + 8 * S
 out = gr = None
-for i in range(12):
+if "--no-gc" in sys.argv:
+    import gc
+
+    gc.disable()
+for i in range(int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 12):
     torch.cuda.synchronize()
     t = time.perf_counter()
+    c = time.process_time()
     out = adaln_forward(xh, sc, sc, 1e-6, check_finite=False)
+    t1 = time.perf_counter()
     gr = adaln_backward_naive(dyh, xh, sc, out.mu, out.rstd, check_finite=False)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t
-    print(json.dumps({"step": i, "ms": round(dt * 1e3, 1), "GBs": round(total / dt / 1e9, 1),
-                      **stats()}), flush=True)
+    print(json.dumps({"step": i, "ms": round(dt * 1e3, 1), "fwd_ms": round((t1 - t) * 1e3, 1),
+                      "cpu_ms": round((time.process_time() - c) * 1e3, 1),
+                      "GBs": round(total / dt / 1e9, 1), **stats()}), flush=True)

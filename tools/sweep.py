@@ -51,6 +51,10 @@ def main():
     ap.add_argument("--which", default="fwd,bwd")
     ap.add_argument("--variants", default="0,1,2,3,4,5,6", help="forward rows variants to time")
     ap.add_argument("--no-ring", action="store_true", help="skip the V/R/smem ring sweep")
+    ap.add_argument("--ring7-cfgs", default="",
+                    help="extra ring-forward configs 'V:R:smemKB,...' (variant 7)")
+    ap.add_argument("--fwd-ring7", action="store_true",
+                    help="sweep V/R/smem of the backward-style ring forward (variant 7)")
     args = ap.parse_args()
     dt, code, es = DT[args.dtype]
     B, S, D = args.batch, args.seq, args.dim
@@ -73,6 +77,12 @@ def main():
         if not args.no_ring:
             cfgs += [dict(V=V, R=R, smem=sm) for V, R, sm in itertools.product(
                 (1, 2, 4), (1, 2, 4), (100 * 1024, 200 * 1024))]
+        for spec in filter(None, args.ring7_cfgs.split(",")):
+            V, R, kb = (int(v) for v in spec.split(":"))
+            cfgs.append(dict(V=V, R=R, smem=kb * 1024, variant=7))
+        if args.fwd_ring7:
+            cfgs += [dict(V=V, R=R, smem=sm, variant=7) for V, R, sm in itertools.product(
+                (0, 1, 2, 4), (0, 1, 2, 4), (0, 100 * 1024, 200 * 1024))]
         for c in cfgs:
             try:
                 nat.set_tuning(0, c.get("V", 0), c.get("R", 0), c.get("smem", 0), False,
