@@ -100,6 +100,37 @@ AL_API int al_adaln_gate_residual_forward(const void* x, const void* f, const vo
                      int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
                      int dtype, double eps, int* nonfinite, void* stream);
 
+/*
+ * Fused Q/K RMSNorm of a packed QKV projection ("Q-Norm + K-Norm"; the
+ * reference names this op only in its design notes, PAPER.md:301 -- there is no reference
+ * implementation, so parity is against a float64 restatement in the tests):
+ *     q_n = q * rsqrt(mean(q^2) + eps) * wq,   k_n = k * rsqrt(mean(k^2) + eps) * wk
+ * over the full width `dim`, q/k/v being the slices [0, dim), [dim, 2 dim), [2 dim, 3 dim) of
+ * each `row_stride`-element row of `qkv` (the [N, 3 dim] output of one projection GEMM).
+ * Writes q_n, k_n ([n_rows, dim] contiguous), optionally a contiguous copy of v (`vc`, NULL to
+ * skip), and rstd [n_rows][2] (fp32; fp64 for fp64).  dim * element size must be a multiple of
+ * 16 bytes and at most 4 KB (dim <= 2048 bf16 / 1024 fp32).
+ */
+AL_API int al_qk_rmsnorm_forward(const void* qkv, int64_t row_stride, const void* wq,
+                          const void* wk, void* qn, void* kn, void* vc, void* rstd,
+                          int64_t n_rows, int64_t dim, int dtype, double eps, int* nonfinite,
+                          void* stream);
+
+/* Scratch bytes al_qk_rmsnorm_backward needs for its per-CTA dwq/dwk partials. */
+AL_API int64_t al_qk_rmsnorm_backward_workspace_bytes(int64_t n_rows, int64_t dim, int dtype);
+
+/*
+ * Backward of al_qk_rmsnorm_forward: writes the whole gradient row of the projection output,
+ * dqkv = [dq | dk | dv] (dv copied from `dv`, the gradient of `vc`; NULL leaves that slice
+ * untouched), and dwq, dwk [dim] (fp32; fp64 for fp64) summed over the rows in a fixed order
+ * (per-CTA partials, then the AdaLN stage-2 kernel): deterministic run to run.
+ */
+AL_API int al_qk_rmsnorm_backward(const void* qkv, int64_t row_stride, const void* wq,
+                           const void* wk, const void* rstd, const void* dqn, const void* dkn,
+                           const void* dv, void* dqkv, void* dwq, void* dwk, void* workspace,
+                           int64_t workspace_bytes, int64_t n_rows, int64_t dim, int dtype,
+                           int* nonfinite, void* stream);
+
 /* Bytes of scratch al_adaln_backward needs for the stage-1 (per-CTA) dscale/dshift partials. */
 AL_API int64_t al_adaln_backward_workspace_bytes(int64_t batch, int64_t seq, int64_t dim,
                                           int64_t mod_stride, int dtype, int64_t n_tile);

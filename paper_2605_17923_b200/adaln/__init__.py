@@ -217,5 +217,5 @@ def activation_bytes(n: int, d: int, element_bytes: int, stat_bytes: int, mode: 
 
 
 from ._gradcheck import DEFAULT_SIZES, GradcheckReport, gradcheck  # noqa: E402
-from .autograd import (FusedAdaLNModulate, FusedGateResidualAdaLN, adaln_modulate,  # noqa: E402,F401
-                       gate_residual_adaln)
+from .autograd import (FusedAdaLNModulate, FusedGateResidualAdaLN, FusedQKRMSNorm,  # noqa: E402,F401
+                       adaln_modulate, gate_residual_adaln, qk_rmsnorm)

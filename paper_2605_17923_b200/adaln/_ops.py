@@ -201,3 +201,74 @@ def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean:
     if own_flag:
         _raise_if_flagged(flag, "dy/x/scale")
     return dx, dscale, dshift
+
+
+# ------------------------------------------------------------------ fused Q/K RMSNorm
+def fused_qk_rmsnorm_forward(qkv: torch.Tensor, wq: torch.Tensor, wk: torch.Tensor,
+                             eps: float = 1e-6, *, copy_v: bool = True,
+                             check_finite: bool = False):
+    """q_n, k_n (, v) = RMSNorm over the full width of the q and k slices of a packed
+    [..., 3D] projection (al_qk_rmsnorm_forward).  Returns (q_n, k_n, v or None, rstd[..., 2])."""
+    if not qkv.is_cuda:
+        raise ShapeMismatch("fused_qk_rmsnorm_forward takes CUDA tensors")
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    if qkv.shape[-1] % 3:
+        raise ShapeMismatch(f"last dim of qkv must be 3 * D, got {qkv.shape[-1]}")
+    d = qkv.shape[-1] // 3
+    if tuple(wq.shape) != (d,) or tuple(wk.shape) != (d,):
+        raise ShapeMismatch(f"wq/wk must have shape ({d},), got {tuple(wq.shape)}, {tuple(wk.shape)}")
+    dev = qkv.device
+    nat.ensure_device(dev.index)
+    qkv = _prep(qkv, qkv.dtype, dev)
+    wq = _prep(wq, qkv.dtype, dev)
+    wk = _prep(wk, qkv.dtype, dev)
+    lead = qkv.shape[:-1]
+    n = qkv.numel() // (3 * d) if qkv.numel() else 0
+    qn = torch.empty(*lead, d, dtype=qkv.dtype, device=dev)
+    kn = torch.empty_like(qn)
+    vc = torch.empty_like(qn) if copy_v else None
+    rstd = torch.empty(*lead, 2, dtype=stat_dtype(qkv.dtype), device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
+    rc = nat.load().al_qk_rmsnorm_forward(
+        qkv.data_ptr(), 3 * d, wq.data_ptr(), wk.data_ptr(), qn.data_ptr(), kn.data_ptr(),
+        vc.data_ptr() if vc is not None else None, rstd.data_ptr(), n, d, dtype_code(qkv.dtype),
+        float(eps), flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
+    nat.check(rc, "al_qk_rmsnorm_forward")
+    _raise_if_flagged(flag, "qkv")
+    return qn, kn, vc, rstd
+
+
+def fused_qk_rmsnorm_backward(qkv: torch.Tensor, wq: torch.Tensor, wk: torch.Tensor,
+                              rstd: torch.Tensor, dqn: torch.Tensor, dkn: torch.Tensor,
+                              dv: torch.Tensor | None = None):
+    """d(qkv) = [dq | dk | dv] and dwq, dwk (fp32; fp64 for fp64) -- al_qk_rmsnorm_backward."""
+    d = qkv.shape[-1] // 3
+    dev = qkv.device
+    nat.ensure_device(dev.index)
+    qkv = _prep(qkv, qkv.dtype, dev)
+    wq = _prep(wq, qkv.dtype, dev)
+    wk = _prep(wk, qkv.dtype, dev)
+    sdt = stat_dtype(qkv.dtype)
+    rstd = _prep(rstd, sdt, dev)
+    dqn = _prep(dqn, qkv.dtype, dev)
+    dkn = _prep(dkn, qkv.dtype, dev)
+    if dv is not None:
+        dv = _prep(dv, qkv.dtype, dev)
+    n = qkv.numel() // (3 * d) if qkv.numel() else 0
+    lib = nat.load()
+    code = dtype_code(qkv.dtype)
+    ws_bytes = lib.al_qk_rmsnorm_backward_workspace_bytes(n, d, code)
+    if ws_bytes < 0:
+        nat.check(nat.AL_ERR_SHAPE, "al_qk_rmsnorm_backward_workspace_bytes")
+    ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
+    dqkv = torch.empty_like(qkv) if dv is not None else torch.zeros_like(qkv)
+    dwq = torch.empty(d, dtype=sdt, device=dev)
+    dwk = torch.empty(d, dtype=sdt, device=dev)
+    rc = lib.al_qk_rmsnorm_backward(
+        qkv.data_ptr(), 3 * d, wq.data_ptr(), wk.data_ptr(), rstd.data_ptr(), dqn.data_ptr(),
+        dkn.data_ptr(), dv.data_ptr() if dv is not None else None, dqkv.data_ptr(),
+        dwq.data_ptr(), dwk.data_ptr(), ws.data_ptr(), int(ws_bytes), n, d, code, None,
+        _stream_ptr(dev))
+    nat.check(rc, "al_qk_rmsnorm_backward")
+    return dqkv, dwq, dwk

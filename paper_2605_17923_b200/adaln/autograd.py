@@ -9,7 +9,8 @@ from __future__ import annotations
 
 import torch
 
-from ._ops import fused_backward, fused_forward, fused_gate_residual_forward
+from ._ops import (fused_backward, fused_forward, fused_gate_residual_forward,
+                   fused_qk_rmsnorm_backward, fused_qk_rmsnorm_forward)
 
 
 class FusedAdaLNModulate(torch.autograd.Function):
@@ -68,3 +69,27 @@ def gate_residual_adaln(x: torch.Tensor, f: torch.Tensor, gate: torch.Tensor, sc
                         shift: torch.Tensor, eps: float = 1e-6):
     """(x + gate * f, LN(x + gate * f) * (1 + scale) + shift), fused forward, composed backward."""
     return FusedGateResidualAdaLN.apply(x, f, gate, scale, shift, eps)
+
+
+class FusedQKRMSNorm(torch.autograd.Function):
+    """(q_n, k_n, v) from a packed [..., 3D] projection: full-width RMSNorm of q and k with
+    weights wq, wk (Wan-2.1's norm_q / norm_k), v passed through contiguous.  One forward and one
+    backward kernel (plus the deterministic dw reduction); the backward writes d(qkv) whole."""
+
+    @staticmethod
+    def forward(ctx, qkv, wq, wk, eps: float = 1e-6):
+        qn, kn, v, rstd = fused_qk_rmsnorm_forward(qkv, wq, wk, eps, copy_v=True)
+        ctx.save_for_backward(qkv, wq, wk, rstd)
+        ctx.w_dtypes = (wq.dtype, wk.dtype)
+        return qn, kn, v
+
+    @staticmethod
+    def backward(ctx, dqn, dkn, dv):
+        qkv, wq, wk, rstd = ctx.saved_tensors
+        dqkv, dwq, dwk = fused_qk_rmsnorm_backward(qkv, wq, wk, rstd, dqn, dkn, dv)
+        return dqkv, dwq.to(ctx.w_dtypes[0]), dwk.to(ctx.w_dtypes[1]), None
+
+
+def qk_rmsnorm(qkv: torch.Tensor, wq: torch.Tensor, wk: torch.Tensor, eps: float = 1e-6):
+    """(RMSNorm(q) * wq, RMSNorm(k) * wk, v) of a packed [..., 3D] qkv projection, fused."""
+    return FusedQKRMSNorm.apply(qkv, wq, wk, eps)

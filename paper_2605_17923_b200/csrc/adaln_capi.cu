@@ -12,6 +12,7 @@
 
 #include "../../include/adaln_b200.h"
 #include "adaln_kernels.cuh"
+#include "qknorm_kernels.cuh"
 
 namespace {
 
@@ -635,11 +636,75 @@ int launch(const Plan& pl, al::FwdParams& p, void* stream, const char* what) {
   return AL_OK;
 }
 
+// ---------------------------------------------------------------- fused Q/K RMSNorm
+constexpr int kQkVpl[] = {1, 2, 3, 4, 6, 8};
+constexpr int kQkNumVpl = 6;
+
+template <typename T>
+const void* qk_kernel_t(bool bwd, int vi) {
+  switch (vi) {
+    case 0: return bwd ? (const void*)al::qk_rms_bwd<T, 1> : (const void*)al::qk_rms_fwd<T, 1>;
+    case 1: return bwd ? (const void*)al::qk_rms_bwd<T, 2> : (const void*)al::qk_rms_fwd<T, 2>;
+    case 2: return bwd ? (const void*)al::qk_rms_bwd<T, 3> : (const void*)al::qk_rms_fwd<T, 3>;
+    case 3: return bwd ? (const void*)al::qk_rms_bwd<T, 4> : (const void*)al::qk_rms_fwd<T, 4>;
+    case 4: return bwd ? (const void*)al::qk_rms_bwd<T, 6> : (const void*)al::qk_rms_fwd<T, 6>;
+    default: return bwd ? (const void*)al::qk_rms_bwd<T, 8> : (const void*)al::qk_rms_fwd<T, 8>;
+  }
+}
+const void* qk_kernel(int dtype, bool bwd, int vi) {
+  switch (dtype) {
+    case AL_BF16: return qk_kernel_t<__nv_bfloat16>(bwd, vi);
+    case AL_F16: return qk_kernel_t<__half>(bwd, vi);
+    case AL_F64: return qk_kernel_t<double>(bwd, vi);
+    default: return qk_kernel_t<float>(bwd, vi);
+  }
+}
+
+// Launch plan shared by the workspace query and the launches: persistent grid of SMs x resident
+// CTAs (capped by rows / warps); the backward keeps per-warp dw accumulators in shared memory,
+// so it runs 8 warps per CTA when they fit in ~110 KB and 4 otherwise.
+int qk_plan(bool bwd, int64_t N, int64_t D, int dtype, Plan* out) {
+  const int es = elem_size(dtype), cs = ct_size(dtype);
+  if (es == 0) return fail(AL_ERR_DTYPE, "unsupported dtype code %d", dtype);
+  if ((D * es) % 16 != 0)
+    return fail(AL_ERR_SHAPE, "qk-norm needs dim * element size to be a multiple of 16 bytes");
+  const int64_t nvec = D * es / 16;
+  if (nvec > 32 * 8)
+    return fail(AL_ERR_SHAPE, "qk-norm supports rows of at most 256 16-byte vectors (D <= %d here)",
+                static_cast<int>(256 * 16 / es));
+  int vi = 0;
+  while (32 * kQkVpl[vi] < nvec) ++vi;
+  int dev, sms;
+  int rc = current_device(&dev);
+  if (!rc) rc = dev_sms(dev, &sms);
+  if (rc) return rc;
+  Plan pl;
+  pl.path = 2;
+  pl.V = kQkVpl[vi];
+  pl.fn = qk_kernel(dtype, bwd, vi);
+  pl.threads = 256;
+  pl.smem = 2 * static_cast<size_t>(D) * cs;
+  if (bwd) {
+    const size_t per_warp = 2 * static_cast<size_t>(D) * cs;
+    if (pl.smem + 8 * per_warp > 110 * 1024) pl.threads = 128;
+    pl.smem += (pl.threads / 32) * per_warp;
+  }
+  int occ = 0;
+  rc = occupancy(pl, dev, &occ);
+  if (rc) return rc;
+  if (occ < 1) return fail(AL_ERR_SHAPE, "qk-norm launch does not fit on this device");
+  const int64_t warps = pl.threads / 32;
+  pl.grid = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(static_cast<int64_t>(sms) * occ, (N + warps - 1) / warps)));
+  *out = pl;
+  return AL_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
-int al_abi_version(void) { return 2; }
+int al_abi_version(void) { return 3; }
 
 const char* al_last_error(void) { return g_err; }
 
@@ -705,6 +770,11 @@ int al_device_init(int device) {
       e = cudaFuncGetAttributes(&fa, resid_generic_kernel(dt));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
     }
+    for (int vi = 0; vi < kQkNumVpl; ++vi)
+      for (bool b : {false, true}) {
+        rc = ensure_attr(qk_kernel(dt, b, vi), device);
+        if (rc) return rc;
+      }
     for (bool vec : {false, true}) {
       cudaFuncAttributes fa;
       e = cudaFuncGetAttributes(&fa, reduce_kernel(dt, vec));
@@ -928,6 +998,113 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
              static_cast<unsigned>(ngroups));
   e = launch_k(rk, rgrid, dim3(1024), rargs, 0, st, kPdlBwd2);
   if (e != cudaSuccess) return cuda_fail(e, "backward stage-2 launch");
+  return AL_OK;
+}
+
+
+int al_qk_rmsnorm_forward(const void* qkv, int64_t row_stride, const void* wq, const void* wk,
+                          void* qn, void* kn, void* vc, void* rstd, int64_t n_rows, int64_t dim,
+                          int dtype, double eps, int* nonfinite, void* stream) {
+  if (n_rows < 0 || dim < 1) return fail(AL_ERR_SHAPE, "n_rows must be >= 0 and dim >= 1");
+  if (!(eps > 0.0)) return fail(AL_ERR_VALUE, "eps must be positive");
+  if (row_stride < (vc ? 3 : 2) * dim)
+    return fail(AL_ERR_SHAPE, "row_stride must cover the q, k (and v) slices");
+  if (n_rows == 0) return AL_OK;
+  if (!qkv || !wq || !wk || !qn || !kn || !rstd) return fail(AL_ERR_SHAPE, "null tensor pointer");
+  const int es = elem_size(dtype);
+  const void* vp[6] = {qkv, wq, wk, qn, kn, vc ? vc : qn};
+  for (const void* q : vp)
+    if (!aligned16(q)) return fail(AL_ERR_SHAPE, "qk-norm tensors must be 16-byte aligned");
+  if (es && (row_stride * es) % 16 != 0) return fail(AL_ERR_SHAPE, "row stride must be 16-byte aligned");
+  Plan pl;
+  int rc = qk_plan(false, n_rows, dim, dtype, &pl);
+  if (rc) return rc;
+  al::QKParams p = {};
+  p.qkv = qkv;
+  p.row_stride = row_stride;
+  p.wq = wq;
+  p.wk = wk;
+  p.qn = qn;
+  p.kn = kn;
+  p.vc = vc;
+  p.rstd = rstd;
+  p.N = n_rows;
+  p.D = dim;
+  p.nvec = static_cast<int>(dim * es / 16);
+  p.G = pl.grid;
+  p.eps = eps;
+  p.nonfinite = nonfinite;
+  void* args[] = {&p};
+  cudaError_t e = launch_k(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem,
+                           static_cast<cudaStream_t>(stream), 0);
+  if (e != cudaSuccess) return cuda_fail(e, "qk-norm forward launch");
+  return AL_OK;
+}
+
+int64_t al_qk_rmsnorm_backward_workspace_bytes(int64_t n_rows, int64_t dim, int dtype) {
+  if (n_rows <= 0 || dim < 1) return n_rows == 0 ? 0 : -1;
+  Plan pl;
+  if (qk_plan(true, n_rows, dim, dtype, &pl)) return -1;
+  return 2 * static_cast<int64_t>(pl.grid) * dim * ct_size(dtype);
+}
+
+int al_qk_rmsnorm_backward(const void* qkv, int64_t row_stride, const void* wq, const void* wk,
+                           const void* rstd, const void* dqn, const void* dkn, const void* dv,
+                           void* dqkv, void* dwq, void* dwk, void* workspace,
+                           int64_t workspace_bytes, int64_t n_rows, int64_t dim, int dtype,
+                           int* nonfinite, void* stream) {
+  if (n_rows < 0 || dim < 1) return fail(AL_ERR_SHAPE, "n_rows must be >= 0 and dim >= 1");
+  if (row_stride < (dv ? 3 : 2) * dim)
+    return fail(AL_ERR_SHAPE, "row_stride must cover the q, k (and v) slices");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int cs = ct_size(dtype), es = elem_size(dtype);
+  if (n_rows == 0) {  // empty batch: the weight gradients are zero
+    if (dwq && dwk) {
+      cudaError_t e = cudaMemsetAsync(dwq, 0, dim * cs, st);
+      if (e == cudaSuccess) e = cudaMemsetAsync(dwk, 0, dim * cs, st);
+      if (e != cudaSuccess) return cuda_fail(e, "memset");
+    }
+    return AL_OK;
+  }
+  if (!qkv || !wq || !wk || !rstd || !dqn || !dkn || !dqkv || !dwq || !dwk)
+    return fail(AL_ERR_SHAPE, "null tensor pointer");
+  const void* vp[7] = {qkv, wq, wk, dqn, dkn, dqkv, dv ? dv : dqn};
+  for (const void* q : vp)
+    if (!aligned16(q)) return fail(AL_ERR_SHAPE, "qk-norm tensors must be 16-byte aligned");
+  if (es && (row_stride * es) % 16 != 0) return fail(AL_ERR_SHAPE, "row stride must be 16-byte aligned");
+  Plan pl;
+  int rc = qk_plan(true, n_rows, dim, dtype, &pl);
+  if (rc) return rc;
+  const int64_t need = 2 * static_cast<int64_t>(pl.grid) * dim * cs;
+  if (!workspace || workspace_bytes < need)
+    return fail(AL_ERR_WORKSPACE, "workspace too small: need %lld bytes", (long long)need);
+  al::QKParams p = {};
+  p.qkv = qkv;
+  p.row_stride = row_stride;
+  p.wq = wq;
+  p.wk = wk;
+  p.rstd = const_cast<void*>(rstd);
+  p.dqn = dqn;
+  p.dkn = dkn;
+  p.dv = dv;
+  p.dqkv = dqkv;
+  p.ws = workspace;
+  p.N = n_rows;
+  p.D = dim;
+  p.nvec = static_cast<int>(dim * es / 16);
+  p.G = pl.grid;
+  p.nonfinite = nonfinite;
+  void* args[] = {&p};
+  cudaError_t e = launch_k(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st, kPdlBwd1);
+  if (e != cudaSuccess) return cuda_fail(e, "qk-norm backward launch");
+  // stage 2: dw_q | dw_k = sum of the G slots, ascending (the AdaLN stage-2 kernel, one group)
+  const void* rk = reduce_kernel(dtype, true);
+  int64_t N64 = n_rows, S64 = n_rows, D64 = dim, G64 = pl.grid, ns = pl.grid;
+  void* rargs[] = {&workspace, &dwq, &dwk, &N64, &S64, &D64, &G64, &ns};
+  const int64_t cols_per_cta = 16 * (16 / cs);
+  e = launch_k(rk, dim3(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta), 1),
+               dim3(1024), rargs, 0, st, kPdlBwd2);
+  if (e != cudaSuccess) return cuda_fail(e, "qk-norm backward stage-2 launch");
   return AL_OK;
 }
 

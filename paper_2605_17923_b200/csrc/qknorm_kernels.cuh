@@ -1,0 +1,275 @@
+// qknorm_kernels.cuh -- fused Q/K RMSNorm of a packed QKV projection (SURVEY.md 8(f) #4,
+// "Q-Norm + K-Norm", the op that sits between the qkv GEMM and attention in a Wan-2.1 block):
+//
+//   q_n = q * rsqrt(mean(q^2) + eps) * w_q,   k_n = k * rsqrt(mean(k^2) + eps) * w_k
+//
+// over the full model width D (Wan's WanRMSNorm(dim) on q and k), reading q and k straight out
+// of the [N, 3D] projection output (row stride 3D) and, optionally, copying v out contiguously,
+// so the block needs no split/contiguous copies.  Backward writes the whole d(qkv) row
+// (dq | dk | dv) and reduces dw_q, dw_k over the rows in two deterministic stages (per-CTA
+// partials here, the cross-CTA sum by adaln_bwd_reduce_vec).
+//
+// Same skeleton as the AdaLN rows kernels: one warp per row, the row's slices held in registers
+// (VPL 16-byte vectors per lane), statistics by warp shuffles only, weights staged in shared
+// memory as fp32 pairs, packed fp32 pair math.  HBM-bound: forward moves 2 N D e in + 2 N D e out
+// (+ v copy), backward 4 N D e in + 2 N D e out (+ v).
+#pragma once
+
+#include "adaln_kernels.cuh"
+
+namespace al {
+
+struct QKParams {
+  const void* qkv;     // [N, row_stride] elements: q at [0, D), k at [D, 2D), v at [2D, 3D)
+  int64_t row_stride;  // elements between rows of qkv / dqkv
+  const void* wq;      // [D]
+  const void* wk;      // [D]
+  void* qn;            // [N, D] forward outputs
+  void* kn;
+  void* vc;            // [N, D] contiguous copy of v (nullable)
+  const void* dqn;     // [N, D] backward inputs
+  const void* dkn;
+  const void* dv;      // [N, D] gradient of vc (nullable: dv slice of dqkv left untouched)
+  void* dqkv;          // [N, row_stride] backward output
+  void* rstd;          // [N, 2] compute type
+  void* ws;            // [2][G][D] compute type: per-CTA dw_q | dw_k partials
+  int64_t N;
+  int64_t D;
+  int nvec;  // D / EPV
+  int G;
+  double eps;
+  int* nonfinite;
+};
+
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256) qk_rms_fwd(const QKParams p) {
+  pdl_enter();
+  using CT = typename Traits<T>::CT;
+  using P = typename PairOf<CT>::type;
+  constexpr int NP = Traits<T>::EPV / 2;
+  extern __shared__ __align__(16) uint8_t smem[];
+  P* wq = reinterpret_cast<P*>(smem);  // [nvec * NP]
+  P* wk = wq + p.nvec * NP;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+  const CT invD = CT(1) / static_cast<CT>(p.D);
+  const CT eps = static_cast<CT>(p.eps);
+  const int64_t RS = p.row_stride * static_cast<int64_t>(sizeof(T));  // bytes between rows
+  const int64_t DB = p.D * static_cast<int64_t>(sizeof(T));
+  bool nf = false;
+
+  for (int c = tid; c < p.nvec; c += blockDim.x) {
+    P a[NP], b[NP];
+    unpack2<T>(__ldg(reinterpret_cast<const uint4*>(p.wq) + c), a);
+    unpack2<T>(__ldg(reinterpret_cast<const uint4*>(p.wk) + c), b);
+#pragma unroll
+    for (int e = 0; e < NP; ++e) {
+      wq[c * NP + e] = a[e];
+      wk[c * NP + e] = b[e];
+    }
+  }
+  __syncthreads();
+
+  for (int64_t row = r0 + warp; row < r1; row += nwarp) {
+    const uint8_t* base = static_cast<const uint8_t*>(p.qkv) + row * RS;
+    uint4 vq[VPL], vk[VPL];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = lane + 32 * i;
+      vq[i] = c < p.nvec ? ld_global_nc_v4(base + c * 16) : make_uint4(0, 0, 0, 0);
+      vk[i] = c < p.nvec ? ld_global_nc_v4(base + DB + c * 16) : make_uint4(0, 0, 0, 0);
+    }
+    CT part[2];
+    {
+      P aq[2] = {splat2(CT(0)), splat2(CT(0))}, ak[2] = {splat2(CT(0)), splat2(CT(0))};
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        P a[NP], b[NP];
+        unpack2<T>(vq[i], a);
+        unpack2<T>(vk[i], b);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          aq[e & 1] = fma2(a[e], a[e], aq[e & 1]);
+          ak[e & 1] = fma2(b[e], b[e], ak[e & 1]);
+        }
+      }
+      const P tq = add2(aq[0], aq[1]), tk = add2(ak[0], ak[1]);
+      part[0] = tq.x + tq.y;
+      part[1] = tk.x + tk.y;
+    }
+    const CT u = warp_reduce_scatter<2>(part, lane);
+    const CT ssq = __shfl_sync(0xffffffffu, u, 0), ssk = __shfl_sync(0xffffffffu, u, 16);
+    const CT rq = CT(1) / sqrt(ssq * invD + eps), rk = CT(1) / sqrt(ssk * invD + eps);
+    const P rq2 = splat2(rq), rk2 = splat2(rk);
+    uint8_t* oq = static_cast<uint8_t*>(p.qn) + row * DB;
+    uint8_t* ok = static_cast<uint8_t*>(p.kn) + row * DB;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < p.nvec) {
+        P a[NP], b[NP];
+        unpack2<T>(vq[i], a);
+        unpack2<T>(vk[i], b);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          a[e] = mul2(mul2(a[e], rq2), wq[c * NP + e]);
+          b[e] = mul2(mul2(b[e], rk2), wk[c * NP + e]);
+        }
+        st_global_cs(oq + c * 16, pack2<T>(a));
+        st_global_cs(ok + c * 16, pack2<T>(b));
+      }
+    }
+    if (p.vc != nullptr) {  // contiguous v for attention: a straight 16-byte copy
+      uint8_t* ov = static_cast<uint8_t*>(p.vc) + row * DB;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        if (c < p.nvec) st_global_cs(ov + c * 16, ld_global_nc_v4(base + 2 * DB + c * 16));
+      }
+    }
+    if (lane == 0) {
+      static_cast<CT*>(p.rstd)[2 * row] = rq;
+      static_cast<CT*>(p.rstd)[2 * row + 1] = rk;
+      nf |= !(finite_ct(ssq) && finite_ct(ssk));
+    }
+  }
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+// Backward.  Per row, for x in {q, k} with r = rstd, xh = x r, g = dy w:
+//   dx = r (g - xh * sum(g xh) / D),     dw += dy xh  (column sums over the rows)
+// Column partials accumulate per warp in shared memory (planar layout, conflict-free 16-byte
+// accesses), are summed over the CTA's warps in a fixed order at the end and written as the
+// CTA's slot of the [2][G][D] workspace.
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256) qk_rms_bwd(const QKParams p) {
+  pdl_enter();
+  using CT = typename Traits<T>::CT;
+  using P = typename PairOf<CT>::type;
+  constexpr int NP = Traits<T>::EPV / 2;
+  constexpr int HP = 16 / static_cast<int>(sizeof(P));  // pairs per 16-byte chunk
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int nvec = p.nvec;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  P* wq = reinterpret_cast<P*>(smem);  // [nvec * NP]
+  P* wk = wq + nvec * NP;
+  P* acc = wk + nvec * NP;  // [nwarp][2 (q, k)][nvec * NP], planar by 16-byte chunk
+  auto ai = [nvec](int w, int which, int c, int e) {
+    return ((w * 2 + which) * (NP / HP) + e / HP) * nvec * HP + c * HP + (e % HP);
+  };
+
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+  const CT invD = CT(1) / static_cast<CT>(p.D);
+  const int64_t RS = p.row_stride * static_cast<int64_t>(sizeof(T));
+  const int64_t DB = p.D * static_cast<int64_t>(sizeof(T));
+  bool nf = false;
+
+  for (int c = tid; c < nvec; c += blockDim.x) {
+    P a[NP], b[NP];
+    unpack2<T>(__ldg(reinterpret_cast<const uint4*>(p.wq) + c), a);
+    unpack2<T>(__ldg(reinterpret_cast<const uint4*>(p.wk) + c), b);
+#pragma unroll
+    for (int e = 0; e < NP; ++e) {
+      wq[c * NP + e] = a[e];
+      wk[c * NP + e] = b[e];
+    }
+  }
+  for (int i = tid; i < nwarp * 2 * nvec * NP; i += blockDim.x) acc[i] = splat2(CT(0));
+  __syncthreads();
+
+  for (int64_t row = r0 + warp; row < r1; row += nwarp) {
+    const uint8_t* base = static_cast<const uint8_t*>(p.qkv) + row * RS;
+    const uint8_t* gq = static_cast<const uint8_t*>(p.dqn) + row * DB;
+    const uint8_t* gk = static_cast<const uint8_t*>(p.dkn) + row * DB;
+    uint4 xq[VPL], xk[VPL], dq[VPL], dk[VPL];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = lane + 32 * i;
+      const bool ok = c < nvec;
+      xq[i] = ok ? ld_global_nc_v4(base + c * 16) : make_uint4(0, 0, 0, 0);
+      xk[i] = ok ? ld_global_nc_v4(base + DB + c * 16) : make_uint4(0, 0, 0, 0);
+      dq[i] = ok ? ld_global_nc_v4(gq + c * 16) : make_uint4(0, 0, 0, 0);
+      dk[i] = ok ? ld_global_nc_v4(gk + c * 16) : make_uint4(0, 0, 0, 0);
+    }
+    const CT rq = static_cast<const CT*>(p.rstd)[2 * row];
+    const CT rk = static_cast<const CT*>(p.rstd)[2 * row + 1];
+    const P rq2 = splat2(rq), rk2 = splat2(rk);
+    // sum(g xh) for q and k; column partials dy * xh
+    CT part[2];
+    {
+      P sq[2] = {splat2(CT(0)), splat2(CT(0))}, sk[2] = {splat2(CT(0)), splat2(CT(0))};
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        if (c < nvec) {
+          P a[NP], b[NP], ga[NP], gb[NP];
+          unpack2<T>(xq[i], a);
+          unpack2<T>(xk[i], b);
+          unpack2<T>(dq[i], ga);
+          unpack2<T>(dk[i], gb);
+#pragma unroll
+          for (int e = 0; e < NP; ++e) {
+            const P xhq = mul2(a[e], rq2), xhk = mul2(b[e], rk2);
+            sq[e & 1] = fma2(mul2(ga[e], wq[c * NP + e]), xhq, sq[e & 1]);
+            sk[e & 1] = fma2(mul2(gb[e], wk[c * NP + e]), xhk, sk[e & 1]);
+            P& aq = acc[ai(warp, 0, c, e)];
+            P& ak = acc[ai(warp, 1, c, e)];
+            aq = fma2(ga[e], xhq, aq);
+            ak = fma2(gb[e], xhk, ak);
+          }
+        }
+      }
+      const P tq = add2(sq[0], sq[1]), tk = add2(sk[0], sk[1]);
+      part[0] = tq.x + tq.y;
+      part[1] = tk.x + tk.y;
+    }
+    const CT u = warp_reduce_scatter<2>(part, lane);
+    const CT mq = __shfl_sync(0xffffffffu, u, 0) * invD, mk = __shfl_sync(0xffffffffu, u, 16) * invD;
+    const P nmq = splat2(-mq), nmk = splat2(-mk);
+    uint8_t* out = static_cast<uint8_t*>(p.dqkv) + row * RS;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < nvec) {
+        P a[NP], b[NP], ga[NP], gb[NP];
+        unpack2<T>(xq[i], a);
+        unpack2<T>(xk[i], b);
+        unpack2<T>(dq[i], ga);
+        unpack2<T>(dk[i], gb);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          // dx = r * (g - xh * m) = r * g - (r * m) * (x * r)
+          a[e] = mul2(fma2(mul2(a[e], rq2), nmq, mul2(ga[e], wq[c * NP + e])), rq2);
+          b[e] = mul2(fma2(mul2(b[e], rk2), nmk, mul2(gb[e], wk[c * NP + e])), rk2);
+        }
+        st_global_cs(out + c * 16, pack2<T>(a));
+        st_global_cs(out + DB + c * 16, pack2<T>(b));
+      }
+    }
+    if (p.dv != nullptr) {
+      const uint8_t* gv = static_cast<const uint8_t*>(p.dv) + row * DB;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        if (c < nvec) st_global_cs(out + 2 * DB + c * 16, ld_global_nc_v4(gv + c * 16));
+      }
+    }
+    if (lane == 0) nf |= !(finite_ct(mq) && finite_ct(mk));
+  }
+  __syncthreads();
+  // this CTA's dw partials: warps summed in ascending order
+  CT* ws = static_cast<CT*>(p.ws);
+  for (int idx = tid; idx < 2 * nvec * NP; idx += blockDim.x) {
+    const int which = idx / (nvec * NP), rem = idx % (nvec * NP), c = rem / NP, e = rem % NP;
+    P s = acc[ai(0, which, c, e)];
+    for (int w = 1; w < nwarp; ++w) s = add2(s, acc[ai(w, which, c, e)]);
+    P* dst = reinterpret_cast<P*>(ws + (static_cast<int64_t>(which) * p.G + k) * p.D) + c * NP + e;
+    *dst = s;
+  }
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+}  // namespace al

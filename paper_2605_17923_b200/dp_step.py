@@ -57,7 +57,8 @@ class WanStyleBlock(nn.Module):
     ``norm_fn(x, scale, shift, eps)`` is the fused LayerNorm-Modulate; the default is the
     sm_100a kernel pair (``adaln_modulate``).  Tests may inject a CPU stand-in to exercise the
     data-parallel host logic on gloo.  With the default norm the attention residual and the
-    second norm run as ONE fused kernel (``gate_residual_adaln``: x + gate1 * proj(a) -> AdaLN).
+    second norm run as ONE fused kernel (``gate_residual_adaln``: x + gate1 * proj(a) -> AdaLN),
+    and Q/K RMSNorm reads q and k straight out of the qkv projection (``qk_rmsnorm``).
     """
 
     def __init__(self, cfg: BlockConfig = BlockConfig(), norm_fn=None):
@@ -67,17 +68,20 @@ class WanStyleBlock(nn.Module):
         self.modulation = nn.Parameter(torch.randn(1, 6, d) / math.sqrt(d))
         self.time_proj = nn.Linear(d, 6 * d)
         self.qkv = nn.Linear(d, 3 * d)
-        self.q_norm = nn.RMSNorm(d // cfg.heads, eps=cfg.eps)
-        self.k_norm = nn.RMSNorm(d // cfg.heads, eps=cfg.eps)
+        # Wan-2.1 norm_q / norm_k: RMSNorm over the full width of q and k
+        self.q_norm = nn.RMSNorm(d, eps=cfg.eps)
+        self.k_norm = nn.RMSNorm(d, eps=cfg.eps)
         self.proj = nn.Linear(d, d)
         self.ffn_in = nn.Linear(d, cfg.ffn)
         self.ffn_out = nn.Linear(cfg.ffn, d)
         self.resid_norm_fn = None
+        self.qk_norm_fn = None
         if norm_fn is None:
-            from .adaln import adaln_modulate, gate_residual_adaln
+            from .adaln import adaln_modulate, gate_residual_adaln, qk_rmsnorm
 
             norm_fn = adaln_modulate
             self.resid_norm_fn = gate_residual_adaln
+            self.qk_norm_fn = qk_rmsnorm
         self.norm_fn = norm_fn
 
     def forward(self, x: torch.Tensor, t_emb: torch.Tensor) -> torch.Tensor:
@@ -86,10 +90,13 @@ class WanStyleBlock(nn.Module):
         e = (self.time_proj(F.silu(t_emb)).view(b, 6, d) + self.modulation).to(x.dtype)
         shift1, scale1, gate1, shift2, scale2, gate2 = e.unbind(1)
         y = self.norm_fn(x, scale1.contiguous(), shift1.contiguous(), self.cfg.eps)
-        q, k, v = self.qkv(y).view(b, s, 3, h, d // h).unbind(2)
-        q = self.q_norm(q).to(v.dtype).transpose(1, 2)
-        k = self.k_norm(k).to(v.dtype).transpose(1, 2)
-        v = v.transpose(1, 2)
+        qkv = self.qkv(y)
+        if self.qk_norm_fn is not None:
+            q, k, v = self.qk_norm_fn(qkv, self.q_norm.weight, self.k_norm.weight, self.cfg.eps)
+        else:
+            q, k, v = qkv.split(d, dim=-1)
+            q, k = self.q_norm(q).to(v.dtype), self.k_norm(k).to(v.dtype)
+        q, k, v = (t.view(b, s, h, d // h).transpose(1, 2) for t in (q, k, v))
         a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(b, s, d)
         if self.resid_norm_fn is not None:
             x, y = self.resid_norm_fn(x, self.proj(a), gate1.contiguous(), scale2.contiguous(),
