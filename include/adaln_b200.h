@@ -100,6 +100,24 @@ AL_API int al_adaln_gate_residual_forward(const void* x, const void* f, const vo
                      int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
                      int dtype, double eps, int* nonfinite, void* stream);
 
+/* Scratch bytes al_gate_residual_backward needs for its per-CTA dgate partials. */
+AL_API int64_t al_gate_residual_backward_workspace_bytes(int64_t batch, int64_t seq, int64_t dim,
+                                                  int64_t mod_stride, int dtype);
+
+/*
+ * Backward of the gated residual of al_adaln_gate_residual_forward: with
+ * G = dxn + gxo (dxn = al_adaln_backward's dx at x_out; gxo = the gradient reaching x_out from
+ * elsewhere, NULL for none), writes dx = G, df = gate (.) G ([batch, seq, dim]) and
+ * dgate = sum over each sample's rows of f (.) G ([batch, dim] at mod_stride, or [dim] when
+ * mod_stride = 0; fp32, fp64 for fp64) -- the last in a fixed order (per-CTA partials, then the
+ * AdaLN stage-2 kernel).  One pass: 3 reads + 2 writes per element.
+ */
+AL_API int al_gate_residual_backward(const void* dxn, const void* gxo, const void* f,
+                              const void* gate, void* dx, void* df, void* dgate,
+                              void* workspace, int64_t workspace_bytes, int64_t batch,
+                              int64_t seq, int64_t dim, int64_t mod_stride, int dtype,
+                              void* stream);
+
 /*
  * Fused Q/K RMSNorm of a packed QKV projection ("Q-Norm + K-Norm"; the
  * reference names this op only in its design notes, PAPER.md:301 -- there is no reference

@@ -22,7 +22,7 @@ LIB = LIBDIR / "libadaln_b200.so"
 
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 SOURCES = ["adaln_capi.cu"]
-HEADERS = ["adaln_kernels.cuh", "qknorm_kernels.cuh", "dtype.cuh", "ptx.cuh"]
+HEADERS = ["adaln_kernels.cuh", "block_kernels.cuh", "dtype.cuh", "ptx.cuh"]
 
 
 def _nvcc() -> str:

@@ -29,7 +29,7 @@ AL_ERR_CUDA = 8
 
 AL_F32, AL_BF16, AL_F16, AL_F64 = 0, 1, 2, 3
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # every symbol include/adaln_b200.h declares: (name, restype, argtypes)
 _i64 = ctypes.c_int64
@@ -46,6 +46,11 @@ _SIGNATURES = {
         ctypes.c_int,
         [_p, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, ctypes.c_int,
          ctypes.c_double, _p, _p],
+    ),
+    "al_gate_residual_backward_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, ctypes.c_int]),
+    "al_gate_residual_backward": (
+        ctypes.c_int,
+        [_p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, _p],
     ),
     "al_qk_rmsnorm_forward": (
         ctypes.c_int,

@@ -272,3 +272,33 @@ def fused_qk_rmsnorm_backward(qkv: torch.Tensor, wq: torch.Tensor, wk: torch.Ten
         _stream_ptr(dev))
     nat.check(rc, "al_qk_rmsnorm_backward")
     return dqkv, dwq, dwk
+
+
+def fused_gate_residual_backward(dxn: torch.Tensor, gxo: torch.Tensor | None, f: torch.Tensor,
+                                 gate: torch.Tensor):
+    """dx = dxn + gxo, df = gate * dx, dgate = sum_s f * dx in one pass
+    (al_gate_residual_backward).  gate: [D] or [B, D]; dgate is fp32 (fp64 for fp64)."""
+    g = geometry(dxn, gate)
+    dev = dxn.device
+    nat.ensure_device(dev.index)
+    dt = dxn.dtype
+    dxn = _prep(dxn, dt, dev)
+    f = _prep(f, dt, dev)
+    gate = _prep(gate, dt, dev)
+    if gxo is not None:
+        gxo = _prep(gxo, dt, dev)
+    lib = nat.load()
+    code = dtype_code(dt)
+    ws_bytes = lib.al_gate_residual_backward_workspace_bytes(g.batch, g.seq, g.dim, g.mod_stride, code)
+    if ws_bytes < 0:
+        nat.check(nat.AL_ERR_SHAPE, "al_gate_residual_backward_workspace_bytes")
+    ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
+    dx = torch.empty_like(dxn)
+    df = torch.empty_like(dxn)
+    dgate = torch.empty(g.grad_shape, dtype=stat_dtype(dt), device=dev)
+    rc = lib.al_gate_residual_backward(
+        dxn.data_ptr(), gxo.data_ptr() if gxo is not None else None, f.data_ptr(),
+        gate.data_ptr(), dx.data_ptr(), df.data_ptr(), dgate.data_ptr(), ws.data_ptr(),
+        int(ws_bytes), g.batch, g.seq, g.dim, g.mod_stride, code, _stream_ptr(dev))
+    nat.check(rc, "al_gate_residual_backward")
+    return dx, df, dgate

@@ -12,7 +12,7 @@
 
 #include "../../include/adaln_b200.h"
 #include "adaln_kernels.cuh"
-#include "qknorm_kernels.cuh"
+#include "block_kernels.cuh"
 
 namespace {
 
@@ -700,11 +700,56 @@ int qk_plan(bool bwd, int64_t N, int64_t D, int dtype, Plan* out) {
   return AL_OK;
 }
 
+// ---------------------------------------------------------------- gated-residual backward
+template <typename T>
+const void* gr_kernel_t(int V) {
+  return V == 1 ? (const void*)al::gate_residual_bwd<T, 1>
+                : (V == 2 ? (const void*)al::gate_residual_bwd<T, 2> : (const void*)al::gate_residual_bwd<T, 4>);
+}
+const void* gr_kernel(int dtype, int V) {
+  switch (dtype) {
+    case AL_BF16: return gr_kernel_t<__nv_bfloat16>(V);
+    case AL_F16: return gr_kernel_t<__half>(V);
+    case AL_F64: return gr_kernel_t<double>(V);
+    default: return gr_kernel_t<float>(V);
+  }
+}
+
+// Column-owner layout: V 16-byte vectors per thread, <= 512 threads; persistent grid of
+// SMs x resident CTAs, capped by the rows.
+int gr_plan(int64_t N, int64_t D, int dtype, Plan* out) {
+  const int es = elem_size(dtype);
+  if (es == 0) return fail(AL_ERR_DTYPE, "unsupported dtype code %d", dtype);
+  if ((D * es) % 16 != 0)
+    return fail(AL_ERR_SHAPE, "gated-residual backward needs dim * element size % 16 == 0");
+  const int64_t nvec = D * es / 16;
+  int V = 1;
+  while (V < 4 && (nvec + V - 1) / V > 512) V *= 2;
+  const int64_t nc = std::max<int64_t>(32, ((nvec + V - 1) / V + 31) / 32 * 32);
+  if (nc > 512) return fail(AL_ERR_SHAPE, "dim too large for the gated-residual backward");
+  int dev, sms;
+  int rc = current_device(&dev);
+  if (!rc) rc = dev_sms(dev, &sms);
+  if (rc) return rc;
+  Plan pl;
+  pl.path = 1;
+  pl.V = V;
+  pl.threads = static_cast<int>(nc);
+  pl.fn = gr_kernel(dtype, V);
+  int occ = 0;
+  rc = occupancy(pl, dev, &occ);
+  if (rc) return rc;
+  if (occ < 1) return fail(AL_ERR_SHAPE, "gated-residual backward launch does not fit");
+  pl.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(sms) * occ, N)));
+  *out = pl;
+  return AL_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
-int al_abi_version(void) { return 3; }
+int al_abi_version(void) { return 4; }
 
 const char* al_last_error(void) { return g_err; }
 
@@ -775,6 +820,10 @@ int al_device_init(int device) {
         rc = ensure_attr(qk_kernel(dt, b, vi), device);
         if (rc) return rc;
       }
+    for (int V : {1, 2, 4}) {
+      rc = ensure_attr(gr_kernel(dt, V), device);
+      if (rc) return rc;
+    }
     for (bool vec : {false, true}) {
       cudaFuncAttributes fa;
       e = cudaFuncGetAttributes(&fa, reduce_kernel(dt, vec));
@@ -1105,6 +1154,77 @@ int al_qk_rmsnorm_backward(const void* qkv, int64_t row_stride, const void* wq, 
   e = launch_k(rk, dim3(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta), 1),
                dim3(1024), rargs, 0, st, kPdlBwd2);
   if (e != cudaSuccess) return cuda_fail(e, "qk-norm backward stage-2 launch");
+  return AL_OK;
+}
+
+
+int64_t al_gate_residual_backward_workspace_bytes(int64_t batch, int64_t seq, int64_t dim,
+                                                  int64_t mod_stride, int dtype) {
+  if (check_common(batch, seq, dim, mod_stride, dtype)) return -1;
+  const int64_t N = batch * seq;
+  if (N == 0) return 0;
+  Plan pl;
+  if (gr_plan(N, dim, dtype, &pl)) return -1;
+  const int64_t ngroups = mod_stride ? batch : 1;
+  return (pl.grid + ngroups - 1) * dim * ct_size(dtype);
+}
+
+int al_gate_residual_backward(const void* dxn, const void* gxo, const void* f, const void* gate,
+                              void* dx, void* df, void* dgate, void* workspace,
+                              int64_t workspace_bytes, int64_t batch, int64_t seq, int64_t dim,
+                              int64_t mod_stride, int dtype, void* stream) {
+  int rc = check_common(batch, seq, dim, mod_stride, dtype);
+  if (rc) return rc;
+  const int64_t N = batch * seq;
+  const int64_t ngroups = mod_stride ? batch : 1;
+  const int cs = ct_size(dtype), es = elem_size(dtype);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (N == 0) {
+    if (dgate) {
+      cudaError_t e = cudaMemsetAsync(dgate, 0, ngroups * dim * cs, st);
+      if (e != cudaSuccess) return cuda_fail(e, "memset");
+    }
+    return AL_OK;
+  }
+  if (!dxn || !f || !gate || !dx || !df || !dgate) return fail(AL_ERR_SHAPE, "null tensor pointer");
+  const void* vp[6] = {dxn, gxo ? gxo : dxn, f, gate, dx, df};
+  for (const void* q : vp)
+    if (!aligned16(q)) return fail(AL_ERR_SHAPE, "gated-residual tensors must be 16-byte aligned");
+  if ((mod_stride * es) % 16 != 0) return fail(AL_ERR_SHAPE, "mod_stride must be 16-byte aligned");
+  Plan pl;
+  rc = gr_plan(N, dim, dtype, &pl);
+  if (rc) return rc;
+  const int64_t nslots = pl.grid + ngroups - 1;
+  const int64_t need = nslots * dim * cs;
+  if (!workspace || workspace_bytes < need)
+    return fail(AL_ERR_WORKSPACE, "workspace too small: need %lld bytes", (long long)need);
+  al::GRParams p = {};
+  p.dxn = dxn;
+  p.gxo = gxo;
+  p.f = f;
+  p.gate = gate;
+  p.dx = dx;
+  p.df = df;
+  p.ws = workspace;
+  p.N = N;
+  p.S_grp = mod_stride ? seq : N;
+  p.D = dim;
+  p.mod_stride = mod_stride;
+  p.nslots = nslots;
+  p.nvec = static_cast<int>(dim * es / 16);
+  p.G = pl.grid;
+  void* args[] = {&p};
+  cudaError_t e = launch_k(pl.fn, dim3(pl.grid), dim3(pl.threads), args, 0, st, kPdlBwd1);
+  if (e != cudaSuccess) return cuda_fail(e, "gated-residual backward launch");
+  const void* rk = reduce_kernel(dtype, true);
+  void* none = nullptr;
+  int64_t G64 = pl.grid, D64 = dim, N64 = N, S64 = p.S_grp, ns = nslots;
+  void* rargs[] = {&workspace, &dgate, &none, &N64, &S64, &D64, &G64, &ns};
+  const int64_t cols_per_cta = 16 * (16 / cs);
+  e = launch_k(rk, dim3(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
+                        static_cast<unsigned>(ngroups)),
+               dim3(1024), rargs, 0, st, kPdlBwd2);
+  if (e != cudaSuccess) return cuda_fail(e, "gated-residual backward stage-2 launch");
   return AL_OK;
 }
 

@@ -1472,9 +1472,10 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce_vec(const CT* __restric
   double a[VE], b[VE];
 #pragma unroll
   for (int e = 0; e < VE; ++e) a[e] = b[e] = 0.0;
+  const bool two = dshift != nullptr;  // dshift == nullptr: reduce the first array only
   if (col < D) {
     const CT* sc = ws + (kf + g) * D + col;
-    const CT* sh = ws + (nslots + kf + g) * D + col;
+    const CT* sh = two ? ws + (nslots + kf + g) * D + col : sc;
     int64_t i = sl;
     for (; i + 192 < n; i += 256) {  // 4 slots x 2 arrays of 16-byte loads in flight
       uint4 va[4], vb[4];
@@ -1517,7 +1518,7 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce_vec(const CT* __restric
     }
   }
   __syncthreads();
-  if (t < 2 * COLS) {
+  if (t < (two ? 2 : 1) * COLS) {
     const int which = t / COLS, c = t % COLS;
     const int64_t oc = static_cast<int64_t>(blockIdx.x) * COLS + c;
     if (oc < D) {
@@ -1545,9 +1546,10 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce(const CT* __restrict__ 
   const int64_t last_row = ((g + 1) * S_grp < N ? (g + 1) * S_grp : N) - 1;
   const int64_t kf = part_owner(first_row, N, G), kl = part_owner(last_row, N, G);
   double a = 0.0, b = 0.0;
+  const bool two = dshift != nullptr;  // dshift == nullptr: reduce the first array only
   if (col < D) {
     const CT* sc = ws + (kf + g) * D + col;
-    const CT* sh = ws + (nslots + kf + g) * D + col;
+    const CT* sh = two ? ws + (nslots + kf + g) * D + col : sc;
     for (int64_t i = w; i <= kl - kf; i += 32) {
       a += static_cast<double>(sc[i * D]);
       b += static_cast<double>(sh[i * D]);

@@ -1,5 +1,7 @@
-// qknorm_kernels.cuh -- fused Q/K RMSNorm of a packed QKV projection (SURVEY.md 8(f) #4,
-// "Q-Norm + K-Norm", the op that sits between the qkv GEMM and attention in a Wan-2.1 block):
+// block_kernels.cuh -- the DiT-block ops adjacent to AdaLN.
+//
+// 1. Fused Q/K RMSNorm of a packed QKV projection ("Q-Norm + K-Norm", the op that sits between
+//    the qkv GEMM and attention in a Wan-2.1 block):
 //
 //   q_n = q * rsqrt(mean(q^2) + eps) * w_q,   k_n = k * rsqrt(mean(k^2) + eps) * w_k
 //
@@ -270,6 +272,118 @@ __global__ void __launch_bounds__(256) qk_rms_bwd(const QKParams p) {
     *dst = s;
   }
   if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+}
+
+// =====================================================================================
+// 2. Backward of the gated residual x_out = x + gate (.) f (the forward is fused into the AdaLN
+//    rows kernel, adaln_fwd_rows<RESID>).  With G = dxn + g_xo (dxn: the AdaLN backward's dx at
+//    x_out, g_xo: the gradient reaching x_out from elsewhere):
+//      dx = G,   df = gate (.) G,   dgate[g, :] = sum over the rows of sample g of f (.) G
+//    Purely elementwise plus a column reduction, so the CTA is laid out like the AdaLN
+//    backward's consumers: thread t owns 16-byte column vectors t + j*nc (j < V) of every row of
+//    the CTA's contiguous row range, the gate of those columns and the dgate partials live in
+//    registers, two rows' loads are in flight per thread, and at each sample boundary the
+//    partials go to the CTA's (slot = CTA + sample) row of a [nslots][D] workspace reduced by
+//    the AdaLN stage-2 kernel -- deterministic.  Reads dxn, g_xo, f; writes dx, df: 5 N D e.
+// =====================================================================================
+struct GRParams {
+  const void* dxn;
+  const void* gxo;  // nullable (zero)
+  const void* f;
+  const void* gate;
+  void* dx;
+  void* df;
+  void* ws;  // [nslots][D] compute type
+  int64_t N, S_grp, D, mod_stride, nslots;
+  int nvec;
+  int G;
+};
+
+template <typename T, int V>
+__global__ void __launch_bounds__(512) gate_residual_bwd(const GRParams p) {
+  pdl_enter();
+  using CT = typename Traits<T>::CT;
+  using P = typename PairOf<CT>::type;
+  constexpr int NP = Traits<T>::EPV / 2;
+  constexpr int RU = 2;  // rows in flight per thread
+  const int nc = blockDim.x, tid = threadIdx.x;
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+  const int64_t RB = p.D * static_cast<int64_t>(sizeof(T));
+  CT* ws = static_cast<CT*>(p.ws);
+  bool own[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) own[j] = tid + j * nc < p.nvec;
+
+  int64_t row0 = r0;
+  while (row0 < r1) {
+    const int64_t g = row0 / p.S_grp;
+    const int64_t seg_end = min(r1, (g + 1) * p.S_grp);
+    P gt[V][NP], acc[V][NP];
+    {
+      const uint4* ga = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(p.gate) +
+                                                       g * p.mod_stride * sizeof(T));
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        unpack2<T>(own[j] ? __ldg(ga + tid + j * nc) : make_uint4(0, 0, 0, 0), gt[j]);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) acc[j][e] = splat2(CT(0));
+      }
+    }
+    for (int64_t row = row0; row < seg_end; row += RU) {
+      uint4 vd[RU][V], vg[RU][V], vf[RU][V];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const bool live = row + u < seg_end;
+        const int64_t ro = (row + u) * RB;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const bool ok = live && own[j];
+          const int64_t off = ro + static_cast<int64_t>(tid + j * nc) * 16;
+          vd[u][j] = ok ? ld_global_nc_v4(static_cast<const uint8_t*>(p.dxn) + off) : make_uint4(0, 0, 0, 0);
+          vg[u][j] = (ok && p.gxo) ? ld_global_nc_v4(static_cast<const uint8_t*>(p.gxo) + off)
+                                   : make_uint4(0, 0, 0, 0);
+          vf[u][j] = ok ? ld_global_nc_v4(static_cast<const uint8_t*>(p.f) + off) : make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        if (row + u < seg_end) {
+          const int64_t ro = (row + u) * RB;
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            if (own[j]) {
+              P a[NP], b[NP], fv[NP];
+              unpack2<T>(vd[u][j], a);
+              unpack2<T>(vg[u][j], b);
+              unpack2<T>(vf[u][j], fv);
+#pragma unroll
+              for (int e = 0; e < NP; ++e) a[e] = add2(a[e], b[e]);  // G in fp32
+              const uint4 Gp = pack2<T>(a);                         // dx, rounded to T
+              unpack2<T>(Gp, a);  // the stored G drives df and dgate, as a composed backward
+#pragma unroll
+              for (int e = 0; e < NP; ++e) {
+                b[e] = mul2(gt[j][e], a[e]);
+                acc[j][e] = fma2(fv[e], a[e], acc[j][e]);
+              }
+              const int64_t off = ro + static_cast<int64_t>(tid + j * nc) * 16;
+              st_global_cs(static_cast<uint8_t*>(p.dx) + off, Gp);
+              st_global_cs(static_cast<uint8_t*>(p.df) + off, pack2<T>(b));
+            }
+          }
+        }
+      }
+    }
+    // this CTA's dgate partial for sample g (each thread owns distinct columns)
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+      if (own[j]) {
+        P* dst = reinterpret_cast<P*>(ws + (k + g) * p.D) + static_cast<int64_t>(tid + j * nc) * NP;
+#pragma unroll
+        for (int e = 0; e < NP; ++e) dst[e] = acc[j][e];
+      }
+    row0 = seg_end;
+  }
 }
 
 }  // namespace al

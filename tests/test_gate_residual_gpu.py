@@ -15,6 +15,7 @@ from conftest import max_rel_err
 from paper_2605_17923_b200 import _native as nat
 from paper_2605_17923_b200.adaln import gate_residual_adaln
 from paper_2605_17923_b200.adaln._ops import (fused_backward, fused_forward,
+                                              fused_gate_residual_backward,
                                               fused_gate_residual_forward)
 from paper_2605_17923_b200.errors import NonFiniteInput, ShapeMismatch
 
@@ -210,3 +211,32 @@ def test_graph_capture(cuda):
     torch.cuda.synchronize()
     for a, b in zip(out, ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float64])
+@pytest.mark.parametrize("shape,per_sample", [((2, 97, 256), True), ((3, 300, 1536), True),
+                                              ((1, 200, 5120), True), ((4, 33, 512), False),
+                                              ((2, 40, 8192), True)])
+def test_residual_backward_kernel_vs_float64(dtype, shape, per_sample, cuda):
+    """al_gate_residual_backward: dx = dxn + gxo, df = gate * dx, dgate = sum_s f * dx."""
+    b, s, d = shape
+    if d * torch.tensor([], dtype=dtype).element_size() > 2048 * 16:
+        pytest.skip("wider than the kernel's 2048 16-byte vectors per row")
+    _, f, gate, _, _ = make(b, s, d, dtype, cuda, seed=s + d, per_sample=per_sample)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    dxn = torch.randn(b, s, d, generator=g).to(dtype).to(cuda)
+    gxo = torch.randn(b, s, d, generator=g).to(dtype).to(cuda)
+    dx, df, dgate = fused_gate_residual_backward(dxn, gxo, f, gate)
+    G = (dxn.double() + gxo.double()).to(dtype).double()  # dx is stored rounded, then drives df/dgate
+    gb = gate.double()[:, None, :] if per_sample else gate.double()
+    tol = TOL[dtype]
+    assert max_rel_err(f64(dx), f64(G)) <= tol
+    assert max_rel_err(f64(df), f64(G * gb)) <= tol
+    ref = (f.double() * G).sum(dim=1 if per_sample else (0, 1))
+    assert max_rel_err(f64(dgate), f64(ref)) <= (1e-11 if dtype == torch.float64 else 1e-5)
+    again = fused_gate_residual_backward(dxn, gxo, f, gate)
+    assert all(torch.equal(a, c) for a, c in zip((dx, df, dgate), again))
+    dx2, _, dgate2 = fused_gate_residual_backward(dxn, None, f, gate)  # no upstream residual grad
+    assert torch.equal(dx2, dxn)
+    assert max_rel_err(f64(dgate2), f64((f.double() * dxn.double()).sum(dim=1 if per_sample else (0, 1)))) <= (
+        1e-11 if dtype == torch.float64 else 1e-5)
