@@ -625,7 +625,61 @@ al::FwdParams fwd_params(const void* x, const void* scale, const void* shift, vo
   p.f = nullptr;
   p.gate = nullptr;
   p.x_out = nullptr;
+  p.sched = nullptr;
+  p.N_static = N;
   return p;
+}
+
+// ---------------------------------------------------------------- dynamic row tail
+// Ticket-counter slot for one dynamically scheduled launch (al::g_sched, zero-initialised
+// module memory; the launch's last CTA re-arms it).  Slots go round-robin, so launches in
+// flight on different streams use different counters as long as fewer than kSchedSlots are
+// outstanding at once.
+std::atomic<unsigned int> g_sched_seq{0};
+
+unsigned int* sched_slot(int dev) {
+  static unsigned int* base[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (base[dev] == nullptr) {
+    void* ptr = nullptr;
+    if (cudaGetSymbolAddress(&ptr, al::g_sched) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return nullptr;
+    }
+    base[dev] = static_cast<unsigned int*>(ptr);
+  }
+  const unsigned int slot = g_sched_seq.fetch_add(1u) % al::kSchedSlots;
+  return base[dev] + 2 * slot;
+}
+
+// Fraction of the rows handed out dynamically by the 16-bit rows forward (the rest is a static
+// even split), capped at one modulation group.  Measured at cfg2 (bf16 D = 5 120, B200,
+// tools/bw_probe.py): forward 5 449 GB/s static, 5 699 / 6 004 / 6 093 / 6 110 / 6 174 GB/s
+// at 0.1 / 0.2 / 0.4 / 0.6 / 0.8.  AL_FWD_DYN overrides (0 disables).
+double fwd_dyn_frac() {
+  static const double f = [] {
+    const char* v = std::getenv("AL_FWD_DYN");
+    return v ? std::atof(v) : 0.8;
+  }();
+  return f;
+}
+
+void enable_dynamic_tail(const Plan& pl, al::FwdParams& p) {
+  const double f = fwd_dyn_frac();
+  if (!(f > 0.0) || pl.path != 2 || pl.R != 2) return;
+  const int64_t warps = static_cast<int64_t>(pl.grid) * (pl.threads / 32);
+  // the tail stays inside the last modulation group (the kernel stages that group once)
+  const int64_t n_dyn = std::min<int64_t>(
+      static_cast<int64_t>(static_cast<double>(p.N) * (f < 1.0 ? f : 1.0)), p.S_grp);
+  // short launches (< 2 tail rows per warp) are one wave anyway: the ticket round trip only
+  // adds latency there (cfg3 S = 3 600: 3 739 vs 3 924 GB/s fwd+bwd)
+  if (n_dyn < 2 * warps) return;
+  int dev;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  unsigned int* slot = sched_slot(dev);
+  if (slot == nullptr) return;
+  p.sched = slot;
+  p.N_static = p.N - n_dyn;
 }
 
 int launch(const Plan& pl, al::FwdParams& p, void* stream, const char* what) {
@@ -751,6 +805,16 @@ extern "C" {
 
 int al_abi_version(void) { return 4; }
 
+#ifdef AL_CTA_TRACE
+// Trace builds only: copy the per-CTA [start, end] globaltimer stamps of the last forward
+// (kernel 0) or backward (kernel 1) launch to host memory.
+AL_API int al_debug_cta_trace(int kernel, unsigned long long* out, int n) {
+  if (n > 2 * 4096) n = 2 * 4096;
+  return cudaMemcpyFromSymbol(out, al::g_cta_trace, n * sizeof(unsigned long long),
+                              kernel * 2 * 4096 * sizeof(unsigned long long)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
 const char* al_last_error(void) { return g_err; }
 
 int al_set_tuning(int kernel, int vecs_per_thread, int rows_per_stage, int smem_budget,
@@ -868,6 +932,7 @@ int al_adaln_forward(const void* x, const void* scale, const void* shift, void* 
   if (rc) return rc;
   al::FwdParams p = fwd_params(x, scale, shift, y, mean, rstd, seq, N, dim, mod_stride, dtype,
                                eps, nonfinite, pl);
+  enable_dynamic_tail(pl, p);
   return launch(pl, p, stream, "forward launch");
 }
 

@@ -27,6 +27,7 @@
 //    partial accumulators are constant within a stage.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "dtype.cuh"
 #include "ptx.cuh"
@@ -54,7 +55,17 @@ struct FwdParams {
   const void* f;
   const void* gate;
   void* x_out;
+  // dynamic tail (adaln_fwd_rows16): rows [N_static, N) are handed out by the ticket counter
+  // sched[0]; sched[1] counts finished CTAs (the last one re-arms both).  nullptr = static only
+  // (N_static == N).
+  unsigned int* sched;
+  int64_t N_static;
 };
+
+// Ticket-counter slots for dynamically scheduled launches; the host hands launches slots
+// round-robin, and the last CTA of each launch resets its slot to zero.
+constexpr int kSchedSlots = 1024;
+__device__ unsigned int g_sched[kSchedSlots][2];
 
 struct BwdParams {
   const void* dy;
@@ -555,8 +566,9 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows2(const FwdParams p) {
 // y = (x - mean) * rstd * (1 + scale) + shift.  About 5 instructions per element instead of 8.
 // =====================================================================================
 template <typename T, int VPL>
-__global__ void __launch_bounds__(256) adaln_fwd_rows16(const FwdParams p) {
+__global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
   pdl_enter();
+  if (threadIdx.x == 0) AL_TRACE(0, 0);
   static_assert(sizeof(T) == 2, "16-bit rows only");
   using P = float2;
   constexpr int NP = 4;  // pairs per 16-byte vector
@@ -573,88 +585,142 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows16(const FwdParams p) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   const int64_t k = blockIdx.x;
-  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+  // static head: rows [0, N_static) split evenly over the CTAs; dynamic tail: rows
+  // [N_static, N) handed out one row per warp from a global ticket counter (p.sched)
+  const int64_t r0 = part_begin(k, p.N_static, p.G), r1 = part_begin(k + 1, p.N_static, p.G);
   const float invD = 1.0f / static_cast<float>(p.D);
   const float eps = static_cast<float>(p.eps);
   const int RB = p.row_bytes;
   bool nf = false;
 
+  auto mod_smem = [&](int c, P* a, P* b) {
+#pragma unroll
+    for (int e = 0; e < NP; ++e) {
+      a[e] = s1[mi(c, e)];
+      b[e] = sh[mi(c, e)];
+    }
+  };
+  // one row by one warp
+  auto do_row = [&](int64_t row) {
+    const uint8_t* xr = static_cast<const uint8_t*>(p.x) + row * RB;
+    uint4 v[VPL];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = lane + 32 * i;
+      v[i] = c < p.nvec ? ld_global_nc_v4(xr + c * 16) : make_uint4(0, 0, 0, 0);
+    }
+    P k0[NP];
+    unpack2<T>(v[0], k0);
+    const float K = __shfl_sync(0xffffffffu, k0[0].x, 0);
+    // pass 1: sum(d), sum(d^2) over valid vectors
+    P s[2] = {splat2(0.0f), splat2(0.0f)}, q[2] = {splat2(0.0f), splat2(0.0f)};
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      if (lane + 32 * i < p.nvec) {
+        const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const P dd = sub16x2_f32<T>(w[e], -K);
+          s[e & 1] = add2(s[e & 1], dd);
+          q[e & 1] = fma2(dd, dd, q[e & 1]);
+        }
+      }
+    }
+    const P ts = add2(s[0], s[1]), tq = add2(q[0], q[1]);
+    const float sd = warp_sum(ts.x + ts.y);
+    const float sq = warp_sum(tq.x + tq.y);
+    const float md = sd * invD;
+    const float m2 = fmaxf(sq - sd * md, 0.0f);
+    const float mean = K + md;
+    const float rs = 1.0f / sqrtf(m2 * invD + eps);
+    const P rs2 = splat2(rs);
+    // pass 2: y = (x - mean) * rstd * (1 + scale) + shift
+    uint8_t* yr = static_cast<uint8_t*>(p.y) + row * RB;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < p.nvec) {
+        const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+        P a[NP], b[NP], o[NP];
+        mod_smem(c, a, b);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) o[e] = fma2(mul2(sub16x2_f32<T>(w[e], -mean), rs2), a[e], b[e]);
+        st_global_cs(yr + c * 16, pack2<T>(o));
+      }
+    }
+    if (lane == 0) {
+      static_cast<float*>(p.mean)[row] = mean;
+      static_cast<float*>(p.rstd)[row] = rs;
+      nf |= !(finite_ct(mean) && finite_ct(sq));
+    }
+  };
+
+  // stage (1 + scale, shift) of group g; the caller brackets it with __syncthreads
+  auto stage_group = [&](int64_t g) {
+    const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
+    const uint8_t* sf = static_cast<const uint8_t*>(p.shift) + g * p.mod_stride * sizeof(T);
+    for (int c = tid; c < p.nvec; c += blockDim.x) {
+      P a[NP], b[NP];
+      unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sc) + c), a);
+      unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sf) + c), b);
+#pragma unroll
+      for (int e = 0; e < NP; ++e) {
+        nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y) && finite_ct(b[e].x) && finite_ct(b[e].y));
+        s1[mi(c, e)] = add2(a[e], splat2(1.0f));
+        sh[mi(c, e)] = b[e];
+      }
+    }
+  };
+
+  int64_t staged = -1;
   int64_t row0 = r0;
   while (row0 < r1) {
     const int64_t g = row0 / p.S_grp;
     const int64_t seg_end = min(r1, (g + 1) * p.S_grp);
     __syncthreads();  // every warp is done with the previous group's modulation
-    {
-      const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
-      const uint8_t* sf = static_cast<const uint8_t*>(p.shift) + g * p.mod_stride * sizeof(T);
-      for (int c = tid; c < p.nvec; c += blockDim.x) {
-        P a[NP], b[NP];
-        unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sc) + c), a);
-        unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sf) + c), b);
-#pragma unroll
-        for (int e = 0; e < NP; ++e) {
-          nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y) && finite_ct(b[e].x) && finite_ct(b[e].y));
-          s1[mi(c, e)] = add2(a[e], splat2(1.0f));
-          sh[mi(c, e)] = b[e];
-        }
-      }
-    }
+    stage_group(g);
     __syncthreads();
-    for (int64_t row = row0 + warp; row < seg_end; row += nwarp) {
-      const uint8_t* xr = static_cast<const uint8_t*>(p.x) + row * RB;
-      uint4 v[VPL];
-#pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        const int c = lane + 32 * i;
-        v[i] = c < p.nvec ? ld_global_nc_v4(xr + c * 16) : make_uint4(0, 0, 0, 0);
-      }
-      P k0[NP];
-      unpack2<T>(v[0], k0);
-      const float K = __shfl_sync(0xffffffffu, k0[0].x, 0);
-      // pass 1: sum(d), sum(d^2) over valid vectors
-      P s[2] = {splat2(0.0f), splat2(0.0f)}, q[2] = {splat2(0.0f), splat2(0.0f)};
-#pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        if (lane + 32 * i < p.nvec) {
-          const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const P dd = sub16x2_f32<T>(w[e], -K);
-            s[e & 1] = add2(s[e & 1], dd);
-            q[e & 1] = fma2(dd, dd, q[e & 1]);
-          }
-        }
-      }
-      const P ts = add2(s[0], s[1]), tq = add2(q[0], q[1]);
-      const float sd = warp_sum(ts.x + ts.y);
-      const float sq = warp_sum(tq.x + tq.y);
-      const float md = sd * invD;
-      const float m2 = fmaxf(sq - sd * md, 0.0f);
-      const float mean = K + md;
-      const float rs = 1.0f / sqrtf(m2 * invD + eps);
-      const P rs2 = splat2(rs);
-      // pass 2: y = (x - mean) * rstd * (1 + scale) + shift
-      uint8_t* yr = static_cast<uint8_t*>(p.y) + row * RB;
-#pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        const int c = lane + 32 * i;
-        if (c < p.nvec) {
-          const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-          P o[NP];
-#pragma unroll
-          for (int e = 0; e < NP; ++e)
-            o[e] = fma2(mul2(sub16x2_f32<T>(w[e], -mean), rs2), s1[mi(c, e)], sh[mi(c, e)]);
-          st_global_cs(yr + c * 16, pack2<T>(o));
-        }
-      }
-      if (lane == 0) {
-        static_cast<float*>(p.mean)[row] = mean;
-        static_cast<float*>(p.rstd)[row] = rs;
-        nf |= !(finite_ct(mean) && finite_ct(sq));
-      }
-    }
+    staged = g;
+    for (int64_t row = row0 + warp; row < seg_end; row += nwarp) do_row(row);
     row0 = seg_end;
   }
+
+  if (p.sched != nullptr) {
+    // Dynamic tail: bandwidth is not shared evenly between SMs once the kernel is
+    // memory-bound (per-CTA end times of a fully static split spread 87..122 us at cfg2), so
+    // the last rows go to whichever warps are free.  The host keeps the tail inside the last
+    // modulation group, staged here once.  The next ticket is requested before the current
+    // row is processed, hiding the atomic's round trip.  Every row runs the same instruction
+    // sequence wherever it lands, so results do not depend on the assignment.
+    const int64_t gl = (p.N - 1) / p.S_grp;
+    if (staged != gl) {
+      __syncthreads();
+      stage_group(gl);
+      __syncthreads();
+    }
+    unsigned int t = 0;
+    if (lane == 0) t = atomicAdd(p.sched, 1u);
+    int64_t row = p.N_static + __shfl_sync(0xffffffffu, t, 0);
+    while (row < p.N) {
+      unsigned int tn = 0;
+      if (lane == 0) tn = atomicAdd(p.sched, 1u);
+      do_row(row);
+      row = p.N_static + __shfl_sync(0xffffffffu, tn, 0);
+    }
+    // the last CTA out re-arms the counter pair for the next launch that draws this slot
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(p.sched + 1, 1u) == static_cast<unsigned int>(p.G - 1)) {
+        atomicExch(p.sched, 0u);
+        atomicExch(p.sched + 1, 0u);
+      }
+    }
+  }
+#ifdef AL_CTA_TRACE
+  __syncthreads();
+  if (tid == 0) AL_TRACE(0, 1);
+#endif
   if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
 }
 
@@ -1193,6 +1259,7 @@ __device__ void fused_stage2(const BwdParams& p, int nc, int tid) {
 template <typename T, int V, int R, bool FULL>
 __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdParams p) {
   pdl_enter();
+  if (threadIdx.x == 0) AL_TRACE(1, 0);
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
   constexpr int EPV = Traits<T>::EPV;
@@ -1270,8 +1337,8 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
   for (int j = 0; j < V; ++j)
 #pragma unroll
     for (int e = 0; e < NP; ++e) acc_sc[j][e] = acc_sh[j][e] = splat2(CT(0));
-  int64_t cur_g = -1;
 
+  int64_t cur_g = -1;
   auto flush = [&](int64_t g) {
     const int64_t slot = k + g;
 #pragma unroll
@@ -1441,6 +1508,10 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
     }
   }
   if (cur_g >= 0) flush(cur_g);
+#ifdef AL_CTA_TRACE
+  named_bar_sync(1, nc);
+  if (tid == 0) AL_TRACE(1, 1);
+#endif
   if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
   if (p.counter != nullptr) fused_stage2<CT>(p, nc, tid);
 }

@@ -105,6 +105,20 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Per-CTA start/end timestamps (%globaltimer, ns) for tail/imbalance studies; compiled only
+// into trace builds (-DAL_CTA_TRACE, tools/ab_variant.sh), read by al_debug_cta_trace.
+#ifdef AL_CTA_TRACE
+__device__ unsigned long long g_cta_trace[2][2 * 4096];
+__device__ __forceinline__ void cta_trace(int kernel, int which) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.x < 4096) g_cta_trace[kernel][2 * blockIdx.x + which] = t;
+}
+#define AL_TRACE(kernel, which) ::al::cta_trace(kernel, which)
+#else
+#define AL_TRACE(kernel, which) ((void)0)
+#endif
+
 // 32-bit shared-window address form: no generic->shared conversion per access.
 __device__ __forceinline__ uint4 ld_shared_v4_u32(uint32_t a) {
   uint4 v;

@@ -1,6 +1,7 @@
 #!/bin/bash
 # Build a kernel variant from a git revision (or a csrc directory) into
 # paper_2605_17923_b200/_lib/variants/<name>.so; select it at run time with AL_LIB_VARIANT=<name>.
+# Extra nvcc flags via $AB_NVCC_FLAGS (e.g. -DAL_CTA_TRACE for the per-CTA timestamp build).
 #   tools/ab_variant.sh <name> <git-rev | csrc-dir>
 set -euo pipefail
 name=$1; src=$2
@@ -16,7 +17,7 @@ else
 fi
 mkdir -p "$root/paper_2605_17923_b200/_lib/variants"
 nvcc -gencode=arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --shared -Xcompiler -fPIC \
-  -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -cudart static \
+  -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -cudart static ${AB_NVCC_FLAGS:-} \
   -o "$root/paper_2605_17923_b200/_lib/variants/$name.so" "$tmp/p/csrc/adaln_capi.cu"
 rm -rf "$tmp"
 echo "built variants/$name.so"
