@@ -62,7 +62,7 @@ extern "C" {
 #define AL_F16 2
 #define AL_F64 3
 
-/* ABI version of this header (bumped on any signature change or addition). */
+/* ABI version of this header (bumped on any signature change or addition): 5. */
 AL_API int al_abi_version(void);
 
 /* Human-readable message for the last error on the calling thread. */
@@ -163,14 +163,20 @@ AL_API int64_t al_adaln_backward_workspace_bytes(int64_t batch, int64_t seq, int
  * d_tile / n_tile: the reference TileConfig (adaln/__init__.py:70-73), validated with the
  * reference bounds (1 <= d_tile <= dim, 1 <= n_tile <= rows per reduction group); n_tile caps
  * the rows per stage-1 partial; 0/0 selects the default tiling (adaln_backward_naive).
+ * flags: AL_BWD_DETERMINISTIC keeps the whole row range statically partitioned, so dscale and
+ * dshift are bit-identical run to run.  Without it (and with 0/0 tiling) the last ~30 % of the
+ * rows (inside the last group) are handed out dynamically to whichever CTA is free, which
+ * balances the SMs' unequal share of HBM bandwidth; dx is unchanged, and the last group's
+ * dscale/dshift then vary at fp32 rounding level with the (timing-dependent) assignment.
  */
+#define AL_BWD_DETERMINISTIC 1
 AL_API int al_adaln_backward(const void* dy, const void* x, const void* scale,
                       const void* mean, const void* rstd,
                       void* dx, void* dscale, void* dshift,
                       void* workspace, int64_t workspace_bytes,
                       int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
                       int dtype, int64_t d_tile, int64_t n_tile,
-                      int* nonfinite, void* stream);
+                      int flags, int* nonfinite, void* stream);
 
 /*
  * Tuning overrides for benchmarking sweeps (0 = automatic).  kernel: 0 = forward, 1 = backward.

@@ -29,7 +29,9 @@ AL_ERR_CUDA = 8
 
 AL_F32, AL_BF16, AL_F16, AL_F64 = 0, 1, 2, 3
 
-ABI_VERSION = 4
+AL_BWD_DETERMINISTIC = 1  # al_adaln_backward flags
+
+ABI_VERSION = 5
 
 # every symbol include/adaln_b200.h declares: (name, restype, argtypes)
 _i64 = ctypes.c_int64
@@ -65,7 +67,7 @@ _SIGNATURES = {
     "al_adaln_backward": (
         ctypes.c_int,
         [_p, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, ctypes.c_int,
-         _i64, _i64, _p, _p],
+         _i64, _i64, ctypes.c_int, _p, _p],
     ),
     "al_set_tuning": (ctypes.c_int, [ctypes.c_int] * 6),
     "al_describe_launch": (

@@ -180,8 +180,10 @@ def _backward(dy, x, scale, mu, rstd, d_tile: int, n_tile: int, check_finite: bo
     sdt = stat_dtype(xd.dtype)
     mud = mud.reshape(g.stats_shape).to(sdt)
     rsd = rsd.reshape(g.stats_shape).to(sdt)
+    # the reference API keeps the reference's fixed per-feature accumulation order
     dx, dscale, dshift = fused_backward(dyd, xd, sc, mud, rsd, d_tile=d_tile, n_tile=n_tile,
-                                        check_finite=check_finite or st.kind != "cuda")
+                                        check_finite=check_finite or st.kind != "cuda",
+                                        deterministic=True)
     return AdalnGrads(dx=st.get(dx), dscale=st.get(dscale), dshift=st.get(dshift))
 
 

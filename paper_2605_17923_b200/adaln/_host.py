@@ -104,7 +104,7 @@ def host_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mu: to
         scb = sc[b0:b1] if per_sample else sc
         nt = min(n_tile, (s1 - s0) if per_sample else (b1 - b0) * (s1 - s0)) if n_tile else 0
         dxd, dsc, dsh = fused_backward(dyd, xd, scb, mud, rsd, d_tile=d_tile if nt else 0,
-                                       n_tile=nt, flag=flag)
+                                       n_tile=nt, flag=flag, deterministic=True)
         parts.append((b0, b1, dsc, dsh))
         side.wait_stream(main)
         with torch.cuda.stream(side):

@@ -164,8 +164,18 @@ def fused_gate_residual_forward(x: torch.Tensor, f: torch.Tensor, gate: torch.Te
 
 def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean: torch.Tensor,
                    rstd: torch.Tensor, *, d_tile: int = 0, n_tile: int = 0,
-                   check_finite: bool = False, flag: torch.Tensor | None = None):
-    """dx, dscale, dshift in one pass over (dy, x) + a deterministic cross-CTA reduction."""
+                   check_finite: bool = False, flag: torch.Tensor | None = None,
+                   deterministic: bool | None = None):
+    """dx, dscale, dshift in one pass over (dy, x) + a fixed-order cross-CTA reduction.
+
+    deterministic: True keeps the static row partition (dscale/dshift bit-identical run to
+    run, the reference's fixed per-feature order); False lets the last ~30 % of the rows go to
+    whichever SM is free (faster: HBM bandwidth is not shared evenly between SMs), which moves
+    the last group's dscale/dshift at fp32 rounding level from run to run -- dx is identical
+    either way.  None (default) follows ``torch.are_deterministic_algorithms_enabled()``.
+    """
+    if deterministic is None:
+        deterministic = torch.are_deterministic_algorithms_enabled()
     if not x.is_cuda:
         raise ShapeMismatch("fused_backward takes CUDA tensors; use adaln_backward_* for host data")
     g = geometry(x, scale)
@@ -196,6 +206,7 @@ def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean:
         dy.data_ptr(), x.data_ptr(), scale.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
         dx.data_ptr(), dscale.data_ptr(), dshift.data_ptr(), ws.data_ptr(), int(ws_bytes),
         g.batch, g.seq, g.dim, g.mod_stride, code, d_tile, n_tile,
+        nat.AL_BWD_DETERMINISTIC if deterministic else 0,
         flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
     nat.check(rc, "al_adaln_backward")
     if own_flag:

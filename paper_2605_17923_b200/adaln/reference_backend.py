@@ -35,7 +35,8 @@ def forward(x, scale, shift, eps):
 
 
 def backward_naive(dy, x, scale, mu, rstd):
-    dx, dscale, dshift = fused_backward(_dev(dy), _dev(x), _dev(scale), _dev(mu), _dev(rstd))
+    dx, dscale, dshift = fused_backward(_dev(dy), _dev(x), _dev(scale), _dev(mu), _dev(rstd),
+                                        deterministic=True)
     return dx.cpu().numpy(), dscale.cpu().numpy(), dshift.cpu().numpy()
 
 
@@ -53,5 +54,5 @@ def dtile_reduce(dy, x, mu, rstd, d_tile, n_tile, fp32_accum):
     x = np.ascontiguousarray(x, dtype=np.float64)
     zero_scale = np.zeros(x.shape[1])
     _, dscale, dshift = fused_backward(_dev(dy), _dev(x), _dev(zero_scale), _dev(mu), _dev(rstd),
-                                       d_tile=int(d_tile), n_tile=int(n_tile))
+                                       d_tile=int(d_tile), n_tile=int(n_tile), deterministic=True)
     return dscale.cpu().numpy(), dshift.cpu().numpy()

@@ -83,6 +83,8 @@ struct Table {
   FwdFn ring[3][3];  // backward-style TMA-ring forward (variant 7)
   BwdFn bwd[3][3];
   BwdFn bwd_full[3][3];  // nvec == V * consumers: ownership predicates compiled out
+  BwdFn bwd_dyn[3][2];   // dynamic-tail instances, R = 2 / 4 (non-deterministic launches)
+  BwdFn bwd_dyn_full[3][2];
   FwdFn fwd_generic;
   BwdFn bwd_generic;
   Table() {
@@ -124,24 +126,36 @@ struct Table {
     ring[2][0] = al::adaln_fwd_ring<T, 4, 1>;
     ring[2][1] = al::adaln_fwd_ring<T, 4, 2>;
     ring[2][2] = al::adaln_fwd_ring<T, 4, 4>;
-    bwd[0][0] = al::adaln_bwd_tma<T, 1, 1, false>;
-    bwd_full[0][0] = al::adaln_bwd_tma<T, 1, 1, true>;
-    bwd[0][1] = al::adaln_bwd_tma<T, 1, 2, false>;
-    bwd_full[0][1] = al::adaln_bwd_tma<T, 1, 2, true>;
-    bwd[0][2] = al::adaln_bwd_tma<T, 1, 4, false>;
-    bwd_full[0][2] = al::adaln_bwd_tma<T, 1, 4, true>;
-    bwd[1][0] = al::adaln_bwd_tma<T, 2, 1, false>;
-    bwd_full[1][0] = al::adaln_bwd_tma<T, 2, 1, true>;
-    bwd[1][1] = al::adaln_bwd_tma<T, 2, 2, false>;
-    bwd_full[1][1] = al::adaln_bwd_tma<T, 2, 2, true>;
-    bwd[1][2] = al::adaln_bwd_tma<T, 2, 4, false>;
-    bwd_full[1][2] = al::adaln_bwd_tma<T, 2, 4, true>;
-    bwd[2][0] = al::adaln_bwd_tma<T, 4, 1, false>;
-    bwd_full[2][0] = al::adaln_bwd_tma<T, 4, 1, true>;
-    bwd[2][1] = al::adaln_bwd_tma<T, 4, 2, false>;
-    bwd_full[2][1] = al::adaln_bwd_tma<T, 4, 2, true>;
-    bwd[2][2] = al::adaln_bwd_tma<T, 4, 4, false>;
-    bwd_full[2][2] = al::adaln_bwd_tma<T, 4, 4, true>;
+    bwd[0][0] = al::adaln_bwd_tma<T, 1, 1, false, false>;
+    bwd_full[0][0] = al::adaln_bwd_tma<T, 1, 1, true, false>;
+    bwd[0][1] = al::adaln_bwd_tma<T, 1, 2, false, false>;
+    bwd_full[0][1] = al::adaln_bwd_tma<T, 1, 2, true, false>;
+    bwd[0][2] = al::adaln_bwd_tma<T, 1, 4, false, false>;
+    bwd_full[0][2] = al::adaln_bwd_tma<T, 1, 4, true, false>;
+    bwd[1][0] = al::adaln_bwd_tma<T, 2, 1, false, false>;
+    bwd_full[1][0] = al::adaln_bwd_tma<T, 2, 1, true, false>;
+    bwd[1][1] = al::adaln_bwd_tma<T, 2, 2, false, false>;
+    bwd_full[1][1] = al::adaln_bwd_tma<T, 2, 2, true, false>;
+    bwd[1][2] = al::adaln_bwd_tma<T, 2, 4, false, false>;
+    bwd_full[1][2] = al::adaln_bwd_tma<T, 2, 4, true, false>;
+    bwd[2][0] = al::adaln_bwd_tma<T, 4, 1, false, false>;
+    bwd_full[2][0] = al::adaln_bwd_tma<T, 4, 1, true, false>;
+    bwd[2][1] = al::adaln_bwd_tma<T, 4, 2, false, false>;
+    bwd_full[2][1] = al::adaln_bwd_tma<T, 4, 2, true, false>;
+    bwd[2][2] = al::adaln_bwd_tma<T, 4, 4, false, false>;
+    bwd_full[2][2] = al::adaln_bwd_tma<T, 4, 4, true, false>;
+    bwd_dyn[0][0] = al::adaln_bwd_tma<T, 1, 2, false, true>;
+    bwd_dyn_full[0][0] = al::adaln_bwd_tma<T, 1, 2, true, true>;
+    bwd_dyn[0][1] = al::adaln_bwd_tma<T, 1, 4, false, true>;
+    bwd_dyn_full[0][1] = al::adaln_bwd_tma<T, 1, 4, true, true>;
+    bwd_dyn[1][0] = al::adaln_bwd_tma<T, 2, 2, false, true>;
+    bwd_dyn_full[1][0] = al::adaln_bwd_tma<T, 2, 2, true, true>;
+    bwd_dyn[1][1] = al::adaln_bwd_tma<T, 2, 4, false, true>;
+    bwd_dyn_full[1][1] = al::adaln_bwd_tma<T, 2, 4, true, true>;
+    bwd_dyn[2][0] = al::adaln_bwd_tma<T, 4, 2, false, true>;
+    bwd_dyn_full[2][0] = al::adaln_bwd_tma<T, 4, 2, true, true>;
+    bwd_dyn[2][1] = al::adaln_bwd_tma<T, 4, 4, false, true>;
+    bwd_dyn_full[2][1] = al::adaln_bwd_tma<T, 4, 4, true, true>;
     fwd_generic = al::adaln_fwd_generic<T>;
     bwd_generic = al::adaln_bwd_generic<T>;
   }
@@ -181,6 +195,14 @@ const void* tma_kernel(int kernel, int dtype, int V, int R, bool full = false, b
   return with_table(dtype, [&](const auto& t) {
     if (kernel) return full ? (const void*)t.bwd_full[a][b] : (const void*)t.bwd[a][b];
     return ring ? (const void*)t.ring[a][b] : (const void*)t.wide[a][b];
+  });
+}
+// dynamic-tail backward instance of a TMA plan (R = 2 or 4 only), or nullptr
+const void* tma_dyn_kernel(int dtype, int V, int R, bool full) {
+  if (R != 2 && R != 4) return nullptr;
+  const int a = vidx(V), b = R == 2 ? 0 : 1;
+  return with_table(dtype, [&](const auto& t) {
+    return full ? (const void*)t.bwd_dyn_full[a][b] : (const void*)t.bwd_dyn[a][b];
   });
 }
 const void* rows_kernel(int dtype, int vi, bool repack) {
@@ -408,7 +430,9 @@ bool ring_plan(int kernel, int dtype, int64_t nvec, int row_bytes, int cs, const
     int64_t ns = budget / stage;
     if (ns > 8) ns = 8;
     if (ns < 2) ns = 2;
-    const size_t extra = 16 * static_cast<size_t>(ns) + (2 * ncw * R * 2 + ncw) * cs + 64;
+    // + per-slot dynamic-tail headers of the backward (row, rows, mean[R], rstd[R])
+    const size_t extra = 16 * static_cast<size_t>(ns) + (2 * ncw * R * 2 + ncw) * cs + 64 +
+                         static_cast<size_t>(ns) * (16 + 2 * R * cs) + 16;
     if (static_cast<size_t>(ns * stage) + extra <= static_cast<size_t>(kSmemOptin)) {
       pl->path = 1;
       pl->V = V;
@@ -664,6 +688,19 @@ double fwd_dyn_frac() {
   return f;
 }
 
+// Backward: fraction of the rows in the dynamic tail (capped at the last group).  Measured at
+// cfg2 (tools/bw_probe.py, B200): backward 5 870 GB/s static (the previous loop; 5 087 for
+// this loop, whose faster CTAs expose the uneven bandwidth split), 5 999 / 6 077 / 6 107 /
+// 6 127 / 6 160 / 6 325 GB/s at 0.15 / 0.2 / 0.3 / 0.5 / 0.8 / 1.0.  AL_BWD_DYN overrides
+// (0 disables).
+double bwd_dyn_frac() {
+  static const double f = [] {
+    const char* v = std::getenv("AL_BWD_DYN");
+    return v ? std::atof(v) : 1.0;
+  }();
+  return f;
+}
+
 void enable_dynamic_tail(const Plan& pl, al::FwdParams& p) {
   const double f = fwd_dyn_frac();
   if (!(f > 0.0) || pl.path != 2 || pl.R != 2) return;
@@ -803,7 +840,7 @@ int gr_plan(int64_t N, int64_t D, int dtype, Plan* out) {
 
 extern "C" {
 
-int al_abi_version(void) { return 4; }
+int al_abi_version(void) { return 5; }
 
 #ifdef AL_CTA_TRACE
 // Trace builds only: copy the per-CTA [start, end] globaltimer stamps of the last forward
@@ -846,6 +883,10 @@ int al_device_init(int device) {
           for (bool full : {false, true}) {
             rc = ensure_attr(tma_kernel(kernel, dt, V, R, full), device);
             if (rc) return rc;
+            if (kernel == 1 && tma_dyn_kernel(dt, V, R, full)) {
+              rc = ensure_attr(tma_dyn_kernel(dt, V, R, full), device);
+              if (rc) return rc;
+            }
             if (kernel == 0) {
               rc = ensure_attr(tma_kernel(kernel, dt, V, R, full, true), device);
               if (rc) return rc;
@@ -1014,15 +1055,16 @@ int64_t al_adaln_backward_workspace_bytes(int64_t batch, int64_t seq, int64_t di
   if (make_plan(1, N, dim, mod_stride, dtype, n_tile, aligned, 1, &pa)) return -1;
   if (make_plan(1, N, dim, mod_stride, dtype, n_tile, aligned, 1, &pg, true)) return -1;
   const int64_t ngroups = mod_stride ? batch : 1;
-  // + 16 bytes: the fused stage-2 grid-barrier counter
-  return 2 * (std::max(pa.grid, pg.grid) + ngroups - 1) * dim * ct_size(dtype) + 16;
+  // static slots (G + groups - 1) + the dynamic tail's G slots; + 16 bytes: the fused stage-2
+  // grid-barrier counter
+  return 2 * (std::max(pa.grid, pg.grid) + ngroups - 1 + pa.grid) * dim * ct_size(dtype) + 16;
 }
 
 int al_adaln_backward(const void* dy, const void* x, const void* scale, const void* mean,
                       const void* rstd, void* dx, void* dscale, void* dshift, void* workspace,
                       int64_t workspace_bytes, int64_t batch, int64_t seq, int64_t dim,
                       int64_t mod_stride, int dtype, int64_t d_tile, int64_t n_tile,
-                      int* nonfinite, void* stream) {
+                      int flags, int* nonfinite, void* stream) {
   int rc = check_common(batch, seq, dim, mod_stride, dtype);
   if (rc) return rc;
   const int64_t N = batch * seq;
@@ -1048,8 +1090,29 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   Plan pl;
   rc = make_plan(1, N, dim, mod_stride, dtype, n_tile, vp, 5, &pl);
   if (rc) return rc;
-  const int64_t nslots = pl.grid + ngroups - 1;
-  const int64_t need = 2 * nslots * dim * ct_size(dtype);
+  const int cs = ct_size(dtype);
+  const bool vec = (dim * cs) % 16 == 0 && aligned16(workspace);
+  Tuning tu;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    tu = g_tune[1];
+  }
+  const int64_t nslots_static = pl.grid + ngroups - 1;
+  // Dynamic tail (see adaln_bwd_tma): TMA path, vector stage 2, no explicit n_tile, not the
+  // cooperative fused stage 2, caller did not ask for AL_BWD_DETERMINISTIC, and at least two
+  // stages per CTA in the tail (which stays inside the last group).
+  int64_t n_dyn = 0;
+  if (pl.path == 1 && vec && n_tile == 0 && tu.variant != 2 && !(flags & AL_BWD_DETERMINISTIC)) {
+    const double f = bwd_dyn_frac();
+    n_dyn = std::min<int64_t>(static_cast<int64_t>(static_cast<double>(N) * (f < 1.0 ? f : 1.0)),
+                              S_grp);
+    // short launches lose more to the second set of partial slots and the ticket traffic than
+    // they gain (cfg3 S = 1 560: 34.2 vs 29.0 us fwd+bwd; break-even near S = 10 000 at
+    // D = 5 120): >= 64 tail rows per CTA
+    if (n_dyn < 64 * static_cast<int64_t>(pl.grid)) n_dyn = 0;
+  }
+  const int64_t nslots = nslots_static + (n_dyn ? pl.grid : 0);
+  const int64_t need = 2 * nslots * dim * cs;
   if (!workspace || workspace_bytes < need) {
     return fail(AL_ERR_WORKSPACE, "workspace too small: need %lld bytes, got %lld",
                 (long long)need, (long long)workspace_bytes);
@@ -1075,22 +1138,29 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   p.counter = nullptr;
   p.dscale = dscale;
   p.dshift = dshift;
-  const int cs = ct_size(dtype);
-  const bool vec = (dim * cs) % 16 == 0 && aligned16(workspace);
+  p.sched = nullptr;
+  p.N_static = N;
+  p.tail_slot0 = -1;
+  if (n_dyn) {
+    int dev;
+    const bool full = pl.threads - 32 == p.nvec / pl.V && p.nvec % pl.V == 0;
+    const void* dfn = tma_dyn_kernel(dtype, pl.V, pl.R, full);
+    unsigned int* slot = nullptr;
+    if (dfn && cudaGetDevice(&dev) == cudaSuccess && ensure_attr(dfn, dev) == AL_OK)
+      slot = sched_slot(dev);
+    if (slot) {
+      pl.fn = dfn;
+      p.sched = slot;
+      p.N_static = N - n_dyn;
+      p.tail_slot0 = nslots_static;
+    }
+  }
   // Fused stage 2: the TMA kernel reduces the partials itself behind a grid barrier, which
   // needs a cooperative launch (all CTAs co-resident) and a zeroed counter at the workspace
   // tail.  Otherwise stage 2 is a second kernel.
-  bool fuse = false;
-  {
-    Tuning tu;
-    {
-      std::lock_guard<std::mutex> lk(g_mu);
-      tu = g_tune[1];
-    }
-    // opt-in (variant 2): measured equal to the separate kernel on B200 (0.189 ms both)
-    fuse = pl.path == 1 && vec && tu.variant == 2 &&
-           workspace_bytes >= need + 16 && cooperative_ok(pl);
-  }
+  // opt-in (variant 2): measured equal to the separate kernel on B200 (0.189 ms both)
+  const bool fuse = pl.path == 1 && vec && tu.variant == 2 &&
+                    workspace_bytes >= need + 16 && cooperative_ok(pl);
   void* args[] = {&p};
   cudaError_t e;
   if (fuse) {
@@ -1106,7 +1176,8 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   // stage 2: 16-byte vector form when every partial row is 16-byte aligned
   const void* rk = reduce_kernel(dtype, vec);
   int64_t G64 = pl.grid;
-  void* rargs[] = {&workspace, &dscale, &dshift, &p.N, &p.S_grp, &p.D, &G64, &p.nslots};
+  void* rargs[] = {&workspace, &dscale, &dshift, &p.N,      &p.S_grp,
+                   &p.D,       &G64,    &p.nslots, &p.N_static, &p.tail_slot0};
   const int64_t cols_per_cta = vec ? 16 * (16 / cs) : 32;
   dim3 rgrid(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
              static_cast<unsigned>(ngroups));
@@ -1214,7 +1285,8 @@ int al_qk_rmsnorm_backward(const void* qkv, int64_t row_stride, const void* wq, 
   // stage 2: dw_q | dw_k = sum of the G slots, ascending (the AdaLN stage-2 kernel, one group)
   const void* rk = reduce_kernel(dtype, true);
   int64_t N64 = n_rows, S64 = n_rows, D64 = dim, G64 = pl.grid, ns = pl.grid;
-  void* rargs[] = {&workspace, &dwq, &dwk, &N64, &S64, &D64, &G64, &ns};
+  int64_t tail0 = -1;
+  void* rargs[] = {&workspace, &dwq, &dwk, &N64, &S64, &D64, &G64, &ns, &N64, &tail0};
   const int64_t cols_per_cta = 16 * (16 / cs);
   e = launch_k(rk, dim3(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta), 1),
                dim3(1024), rargs, 0, st, kPdlBwd2);
@@ -1284,7 +1356,8 @@ int al_gate_residual_backward(const void* dxn, const void* gxo, const void* f, c
   const void* rk = reduce_kernel(dtype, true);
   void* none = nullptr;
   int64_t G64 = pl.grid, D64 = dim, N64 = N, S64 = p.S_grp, ns = nslots;
-  void* rargs[] = {&workspace, &dgate, &none, &N64, &S64, &D64, &G64, &ns};
+  int64_t tail0 = -1;
+  void* rargs[] = {&workspace, &dgate, &none, &N64, &S64, &D64, &G64, &ns, &N64, &tail0};
   const int64_t cols_per_cta = 16 * (16 / cs);
   e = launch_k(rk, dim3(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
                         static_cast<unsigned>(ngroups)),

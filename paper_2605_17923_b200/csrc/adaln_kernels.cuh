@@ -90,6 +90,12 @@ struct BwdParams {
   unsigned int* counter;
   void* dscale;
   void* dshift;
+  // dynamic tail (adaln_bwd_tma): rows [N_static, N), all in the last group, go out one stage
+  // per ticket from sched[0] (sched[1] counts finished CTAs; the last re-arms both); CTA k's
+  // tail partials land in slot tail_slot0 + k.  sched == nullptr: static only (N_static == N).
+  unsigned int* sched;
+  int64_t N_static;
+  int64_t tail_slot0;
 };
 
 // Row partition shared by stage 1 and stage 2.
@@ -1255,8 +1261,17 @@ __device__ void fused_stage2(const BwdParams& p, int nc, int tid) {
 // xhat = (x - mu) * rstd and g = dy * (1 + scale) once, keeps both in registers across the
 // row-sum barrier, folds dy and dy*xhat into its column accumulators, and after the barrier
 // writes dx = rstd * (g - mean(g) - xhat * mean(g*xhat)).  Packed fp32 pair math.
+//
+// Static head + optional dynamic tail (p.sched != nullptr): rows [0, N_static) are split
+// evenly over the CTAs, accumulated per (CTA, group) into slot k + g (deterministic).  Rows
+// [N_static, N) -- inside the last group -- are handed out one stage at a time by a global
+// ticket counter that the producer lane draws from; the producer passes each stage's row
+// index, count and statistics to the consumers in a per-stage header next to the ring.  The
+// tail's partials go to the CTA's tail slot tail_slot0 + k; their sum order depends on which
+// CTA drew which stage, so dscale/dshift of the last group are reproducible only to fp32
+// rounding in this mode (dx is bit-identical either way).
 // =====================================================================================
-template <typename T, int V, int R, bool FULL>
+template <typename T, int V, int R, bool FULL, bool DYN>
 __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdParams p) {
   pdl_enter();
   if (threadIdx.x == 0) AL_TRACE(1, 0);
@@ -1275,9 +1290,17 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(NS) * stage_bytes);
   uint64_t* empty = full + NS;
   CT* red = reinterpret_cast<CT*>(empty + NS);  // [2][ncw][R][2] : (sum g, sum g*xhat)
+  // dynamic-tail stage headers: row, rows, mean[R], rstd[R] per ring slot
+  int64_t* h_row = reinterpret_cast<int64_t*>(
+      (reinterpret_cast<uintptr_t>(red + 2 * ncw * R * 2) + 7) & ~uintptr_t(7));
+  int* h_n = reinterpret_cast<int*>(h_row + NS);
+  CT* h_m = reinterpret_cast<CT*>(
+      (reinterpret_cast<uintptr_t>(h_n + NS) + 7) & ~uintptr_t(7));
+  CT* h_r = h_m + NS * R;
 
   const int64_t k = blockIdx.x;
-  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+  const int64_t r0 = part_begin(k, p.N_static, p.G), r1 = part_begin(k + 1, p.N_static, p.G);
+  const bool dyn = DYN && p.sched != nullptr;
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -1297,10 +1320,7 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       w.init(r0, r1, p.S_grp);
       int s = 0;
       uint32_t f = 0;
-      while (!w.done()) {
-        int64_t start, g;
-        const int rows = w.next(R, start, g);
-        if (f > 0) mbar_wait(&empty[s], (f - 1) & 1);
+      auto issue = [&](int64_t start, int rows) {
         mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(2 * rows * RB));
         uint8_t* dst = smem + static_cast<size_t>(s) * stage_bytes;
         for (int rr = 0; rr < rows; ++rr) {
@@ -1310,6 +1330,51 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
         if (++s == NS) {
           s = 0;
           ++f;
+        }
+      };
+      while (!w.done()) {
+        int64_t start, g;
+        const int rows = w.next(R, start, g);
+        if (f > 0) mbar_wait(&empty[s], (f - 1) & 1);
+        issue(start, rows);
+      }
+      if (dyn) {
+        // tickets and their statistics are fetched one stage ahead, so neither the atomic's
+        // nor the loads' round trip sits between two stage issues
+        const CT* mean_p = static_cast<const CT*>(p.mean);
+        const CT* rstd_p = static_cast<const CT*>(p.rstd);
+        auto stats = [&](int64_t start, CT* m, CT* r) {
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const bool ok = start + rr < p.N;
+            m[rr] = ok ? mean_p[start + rr] : CT(0);
+            r[rr] = ok ? rstd_p[start + rr] : CT(0);
+          }
+        };
+        int64_t start = p.N_static + static_cast<int64_t>(atomicAdd(p.sched, 1u)) * R;
+        CT m[R], r[R];
+        stats(start, m, r);
+        unsigned int tn = atomicAdd(p.sched, 1u);
+        while (true) {
+          const int rows = start < p.N ? static_cast<int>(p.N - start < R ? p.N - start : R) : 0;
+          if (f > 0) mbar_wait(&empty[s], (f - 1) & 1);
+          h_row[s] = start;
+          h_n[s] = rows;
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            h_m[s * R + rr] = m[rr];
+            h_r[s * R + rr] = r[rr];
+          }
+          if (rows == 0) {  // end marker: completes the slot's phase without data
+            mbar_arrive(&full[s]);
+            break;
+          }
+          issue(start, rows);
+          start = p.N_static + static_cast<int64_t>(tn) * R;
+          if (start < p.N) {
+            stats(start, m, r);
+            tn = atomicAdd(p.sched, 1u);
+          }
         }
       }
     }
@@ -1338,9 +1403,7 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
 #pragma unroll
     for (int e = 0; e < NP; ++e) acc_sc[j][e] = acc_sh[j][e] = splat2(CT(0));
 
-  int64_t cur_g = -1;
-  auto flush = [&](int64_t g) {
-    const int64_t slot = k + g;
+  auto flush = [&](int64_t slot) {
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       if (vmask >> j & 1) {
@@ -1356,7 +1419,197 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       }
     }
   };
+  auto load_scale = [&](int64_t g) {
+    const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (vmask >> j & 1) {
+        unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sc + coff[j])), s1[j]);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) s1[j][e] = add2(s1[j][e], splat2(CT(1)));
+      } else {
+#pragma unroll
+        for (int e = 0; e < NP; ++e) s1[j][e] = splat2(CT(0));
+      }
+    }
+  };
 
+  if constexpr (DYN) {
+  int s = 0;
+  uint32_t ph = 0;
+  int it = 0;
+
+  // One ring stage (the caller has waited on full[s]): `rows` rows from rb, statistics in
+  // mc/rc.  ALL (compile time) = the stage holds R rows, so no row predicates or zero fills
+  // are emitted on the common path; short stages take the predicated instance.
+  auto stage = [&](auto all_tag, int64_t rb, int rows, const CT* mc, const CT* rc) {
+    constexpr bool ALL = decltype(all_tag)::value;
+    // 32-bit shared-window addresses: no generic->shared conversion per load (+1.3 %)
+    const uint32_t stx_u = smem_addr(smem) + static_cast<uint32_t>(s * stage_bytes);
+    const uint32_t std_u = stx_u + static_cast<uint32_t>(R * RB);
+    CT* rd = red + (it & 1) * (ncw * R * 2);
+
+    // phase 1: row sums of g and g*xhat; column accumulators of dy and dy*xhat.
+    // Rows past `rows` (stage tail) and columns past D read as zero, so every lane runs the
+    // same instruction stream and the shuffles below are convergent.
+    P xh[R][V][NP], gg[R][V][NP];
+    CT rowsum[R * 2];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const bool live = ALL || rr < rows;
+      const P nm = splat2(-mc[rr]), r2 = splat2(rc[rr]);
+      // 16-bit inputs: xhat = x*r - m*r in one FFMA2 (the product is exact inside the FMA;
+      // the absolute error ~|m| r 2^-24 is far below the inputs' own 2^-9 rounding)
+      const P nmr = splat2(-mc[rr] * rc[rr]);
+      // two accumulators per row sum break the FADD2/FFMA2 dependency chains
+      P sg[2] = {splat2(CT(0)), splat2(CT(0))}, sgx[2] = {splat2(CT(0)), splat2(CT(0))};
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const bool ok = live && (vmask >> j & 1);
+        P xv[NP], dv[NP];
+        const uint32_t o = static_cast<uint32_t>(rr * RB + coff[j]);
+        unpack2<T>(ok ? ld_shared_v4_u32(stx_u + o) : make_uint4(0, 0, 0, 0), xv);
+        unpack2<T>(ok ? ld_shared_v4_u32(std_u + o) : make_uint4(0, 0, 0, 0), dv);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          if constexpr (sizeof(T) == 2) xh[rr][j][e] = fma2(xv[e], r2, nmr);
+          else xh[rr][j][e] = mul2(add2(xv[e], nm), r2);
+          gg[rr][j][e] = mul2(dv[e], s1[j][e]);
+          sg[e & 1] = add2(sg[e & 1], gg[rr][j][e]);
+          sgx[e & 1] = fma2(gg[rr][j][e], xh[rr][j][e], sgx[e & 1]);
+          acc_sh[j][e] = add2(acc_sh[j][e], dv[e]);
+          acc_sc[j][e] = fma2(dv[e], xh[rr][j][e], acc_sc[j][e]);
+        }
+      }
+      const P tsg = add2(sg[0], sg[1]), tsgx = add2(sgx[0], sgx[1]);
+      rowsum[2 * rr] = tsg.x + tsg.y;
+      rowsum[2 * rr + 1] = tsgx.x + tsgx.y;
+    }
+    {
+      constexpr int NV = 2 * R, GRP = 32 / NV;
+      const CT u = warp_reduce_scatter<NV>(rowsum, lane);
+      if ((lane & (GRP - 1)) == 0) rd[warp * NV + lane / GRP] = u;
+    }
+    named_bar_sync(1, nc);
+    // every consumer has read this stage into registers: release the slot to the producer
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+
+    // cross-warp totals, spread over the lanes: rd holds ncw x NV values [warp][k]; lane l
+    // sums entries l, l+32, ... (all of index k = l % NV), lanes of equal k are combined by a
+    // butterfly, and every thread then reads the NV totals by shuffles.  Fixed order ->
+    // deterministic; ~2 shared loads + 3 + NV shuffles instead of ncw * NV loads per thread.
+    CT tot[2 * R];
+    {
+      constexpr int NV = 2 * R;
+      const int nval = ncw * NV;
+      CT s_l = CT(0);
+      for (int i = lane; i < nval; i += 32) s_l += rd[i];
+#pragma unroll
+      for (int off = NV; off < 32; off <<= 1) s_l += __shfl_xor_sync(0xffffffffu, s_l, off);
+#pragma unroll
+      for (int q = 0; q < NV; ++q) tot[q] = __shfl_sync(0xffffffffu, s_l, q);
+    }
+
+    // phase 2: dx = rstd * (g - mean(g) - xhat * mean(g*xhat))
+    uint8_t* dxrow = static_cast<uint8_t*>(p.dx) + rb * RB;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (ALL || rr < rows) {
+        // dx = r*g - r*mean(g) - (r*mean(g*xhat)) * xhat: two FFMA2 per pair
+        const CT rr_ = rc[rr];
+        const P c0 = splat2(-rr_ * tot[2 * rr] * invD), c1 = splat2(-rr_ * tot[2 * rr + 1] * invD);
+        const P r2 = splat2(rr_);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if (vmask >> j & 1) {
+            P o[NP];
+#pragma unroll
+            for (int e = 0; e < NP; ++e)
+              o[e] = fma2(gg[rr][j][e], r2, fma2(xh[rr][j][e], c1, c0));
+            st_global_cs(dxrow + rr * RB + coff[j], pack2<T>(o));
+          }
+        }
+        if (tid == 0) nf |= !(finite_ct(tot[2 * rr]) && finite_ct(tot[2 * rr + 1]));
+      }
+    }
+    if (++s == NS) {
+      s = 0;
+      ph ^= 1;
+    }
+    ++it;
+  };
+
+  // Static head.  Segments = the CTA's rows of one reduction group (sample): (1+scale) loaded
+  // once, then full R-row stages, one predicated tail stage, and the group's partials flushed
+  // to slot k + g.  Statistics are prefetched one stage ahead.  The producer's StageWalker
+  // issues the same sequence.
+  int64_t row = r0;
+  while (row < r1) {
+    const int64_t g = row / p.S_grp;
+    const int64_t seg_end = min((g + 1) * p.S_grp, r1);
+    const int n = static_cast<int>(seg_end - row);
+    load_scale(g);
+    const CT* mp = mean_p + row;
+    const CT* rp = rstd_p + row;
+    CT mc[R], rc[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      mc[rr] = rr < n ? mp[rr] : CT(0);
+      rc[rr] = rr < n ? rp[rr] : CT(0);
+    }
+    const int nfull = n / R;
+    for (int i = 0; i < nfull; ++i) {
+      CT mn[R], rn[R];
+      const int nx = (i + 1) * R, left = n - nx;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        mn[rr] = rr < left ? mp[nx + rr] : CT(0);
+        rn[rr] = rr < left ? rp[nx + rr] : CT(0);
+      }
+      mbar_wait(&full[s], ph);
+      stage(std::true_type{}, row + i * R, R, mc, rc);
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        mc[rr] = mn[rr];
+        rc[rr] = rn[rr];
+      }
+    }
+    if (n > nfull * R) {
+      mbar_wait(&full[s], ph);
+      stage(std::false_type{}, row + nfull * R, n - nfull * R, mc, rc);
+    }
+    flush(k + g);
+    row = seg_end;
+  }
+
+  if (dyn) {
+    // Dynamic tail (last group): stages arrive in whatever order the tickets fall; an empty
+    // header ends the stream.  The CTA's tail partial always goes to its tail slot (zeros if it
+    // drew nothing), which stage 2 adds after the group's static slots.
+    load_scale((p.N - 1) / p.S_grp);
+    while (true) {
+      mbar_wait(&full[s], ph);
+      const int64_t rb = h_row[s];
+      const int rows = h_n[s];
+      if (rows == 0) break;
+      CT mc[R], rc[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        mc[rr] = h_m[s * R + rr];
+        rc[rr] = h_r[s * R + rr];
+      }
+      if (rows == R) stage(std::true_type{}, rb, R, mc, rc);
+      else stage(std::false_type{}, rb, rows, mc, rc);
+    }
+    flush(p.tail_slot0 + k);
+  }
+  } else {
+    // Static-only instance (deterministic launches): the predicated single-instance loop.  Its
+    // CTAs stay issue-bound at one common rate; the leaner DYN loop makes them memory-bound
+    // and, without the dynamic tail, exposes the uneven split of HBM bandwidth between SMs
+    // (cfg2: 5 870 vs 5 087 GB/s).
+  int64_t cur_g = -1;
   StageWalker w;
   w.init(r0, r1, p.S_grp);
   int s = 0;
@@ -1390,7 +1643,7 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       }
     }
     if (g != cur_g) {
-      if (cur_g >= 0) flush(cur_g);
+      if (cur_g >= 0) flush(k + cur_g);
       cur_g = g;
       const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
 #pragma unroll
@@ -1507,12 +1760,24 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       rcur[rr] = rnext[rr];
     }
   }
-  if (cur_g >= 0) flush(cur_g);
+  if (cur_g >= 0) flush(k + cur_g);
+  }
 #ifdef AL_CTA_TRACE
   named_bar_sync(1, nc);
   if (tid == 0) AL_TRACE(1, 1);
 #endif
   if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+  if (dyn) {
+    // the last CTA out re-arms the ticket pair (consumers only: the producer has returned)
+    named_bar_sync(1, nc);
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(p.sched + 1, 1u) == static_cast<unsigned int>(p.G - 1)) {
+        atomicExch(p.sched, 0u);
+        atomicExch(p.sched + 1, 0u);
+      }
+    }
+  }
   if (p.counter != nullptr) fused_stage2<CT>(p, nc, tid);
 }
 
@@ -1528,7 +1793,8 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce_vec(const CT* __restric
                                                              CT* __restrict__ dscale,
                                                              CT* __restrict__ dshift, int64_t N,
                                                              int64_t S_grp, int64_t D, int64_t G,
-                                                             int64_t nslots) {
+                                                             int64_t nslots, int64_t Ns,
+                                                             int64_t tail0) {
   pdl_enter();
   constexpr int VE = 16 / sizeof(CT);  // columns per 16-byte vector
   constexpr int COLS = 16 * VE;        // columns per CTA
@@ -1536,10 +1802,18 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce_vec(const CT* __restric
   const int t = threadIdx.x, hl = t & 15, sl = t >> 4, warp = t >> 5;
   const int64_t g = blockIdx.y;
   const int64_t col = static_cast<int64_t>(blockIdx.x) * COLS + hl * VE;
+  // slots of group g: the static owners of its rows below Ns (slot k + g, ascending k), then --
+  // for the last group of a dynamically scheduled launch -- the G tail slots tail0 + k
   const int64_t first_row = g * S_grp;
-  const int64_t last_row = ((g + 1) * S_grp < N ? (g + 1) * S_grp : N) - 1;
-  const int64_t kf = part_owner(first_row, N, G), kl = part_owner(last_row, N, G);
-  const int64_t n = kl - kf + 1;
+  const int64_t end_row = (g + 1) * S_grp < N ? (g + 1) * S_grp : N;
+  const int64_t last_static = (end_row < Ns ? end_row : Ns) - 1;
+  int64_t kf = 0, n1 = 0;
+  if (first_row <= last_static) {
+    kf = part_owner(first_row, Ns, G);
+    n1 = part_owner(last_static, Ns, G) - kf + 1;
+  }
+  const int64_t n2 = (tail0 >= 0 && end_row == N) ? G : 0;
+  const int64_t n = n1 + n2;
   double a[VE], b[VE];
 #pragma unroll
   for (int e = 0; e < VE; ++e) a[e] = b[e] = 0.0;
@@ -1547,13 +1821,16 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce_vec(const CT* __restric
   if (col < D) {
     const CT* sc = ws + (kf + g) * D + col;
     const CT* sh = two ? ws + (nslots + kf + g) * D + col : sc;
+    // slot i -> row offset (in units of D) from sc / sh
+    const int64_t jump = tail0 - (kf + g) - n1;
+    auto off = [&](int64_t i) { return (i < n1 ? i : i + jump) * D; };
     int64_t i = sl;
     for (; i + 192 < n; i += 256) {  // 4 slots x 2 arrays of 16-byte loads in flight
       uint4 va[4], vb[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        va[u] = __ldg(reinterpret_cast<const uint4*>(sc + (i + 64 * u) * D));
-        vb[u] = __ldg(reinterpret_cast<const uint4*>(sh + (i + 64 * u) * D));
+        va[u] = __ldg(reinterpret_cast<const uint4*>(sc + off(i + 64 * u)));
+        vb[u] = __ldg(reinterpret_cast<const uint4*>(sh + off(i + 64 * u)));
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -1567,8 +1844,8 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce_vec(const CT* __restric
       }
     }
     for (; i < n; i += 64) {
-      const uint4 va = __ldg(reinterpret_cast<const uint4*>(sc + i * D));
-      const uint4 vb = __ldg(reinterpret_cast<const uint4*>(sh + i * D));
+      const uint4 va = __ldg(reinterpret_cast<const uint4*>(sc + off(i)));
+      const uint4 vb = __ldg(reinterpret_cast<const uint4*>(sh + off(i)));
       const CT* pa = reinterpret_cast<const CT*>(&va);
       const CT* pb = reinterpret_cast<const CT*>(&vb);
 #pragma unroll

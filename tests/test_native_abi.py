@@ -53,7 +53,7 @@ def test_abi_version_and_errors_without_gpu():
                                 1e-6, None, None) == nat.AL_OK
     # tile bounds use the reference's InvalidTile rule
     rc = lib.al_adaln_backward(None, None, None, None, None, None, None, None, None, 0,
-                               1, 4, 8, 0, nat.AL_F32, 9, 1, None, None)
+                               1, 4, 8, 0, nat.AL_F32, 9, 1, 0, None, None)
     assert rc == nat.AL_ERR_TILE
 
 
