@@ -21,8 +21,13 @@ LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libadaln_b200.so"
 
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
-SOURCES = ["adaln_capi.cu"]
-HEADERS = ["adaln_kernels.cuh", "block_kernels.cuh", "dtype.cuh", "ptx.cuh"]
+# adaln_capi.cu (C ABI, planning, launches) + one kernel-instantiation TU per dtype, compiled in
+# parallel and linked into one library (tools/gen_instances.py writes the instance lists)
+SOURCES = ["adaln_capi.cu", "instances_f32.cu", "instances_bf16.cu", "instances_f16.cu",
+           "instances_f64.cu"]
+HEADERS = ["adaln_kernels.cuh", "block_kernels.cuh", "dtype.cuh", "ptx.cuh", "instances_extern.inc"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+         "--expt-relaxed-constexpr", "-diag-suppress", "20279,20281"]
 
 
 def _nvcc() -> str:
@@ -45,18 +50,31 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale(LIB, deps):
         return LIB
     LIBDIR.mkdir(exist_ok=True)
+    objdir = LIBDIR / "obj"
+    objdir.mkdir(exist_ok=True)
+    nvcc = _nvcc()
+    procs = []
+    for src in SOURCES:
+        obj = objdir / (Path(src).stem + ".o")
+        cmd = [nvcc, ARCH, *FLAGS, "-Xptxas", "-v", "-c", "-o", str(obj), str(CSRC / src)]
+        procs.append((src, obj, subprocess.Popen(cmd, cwd=str(CSRC), stdout=subprocess.PIPE,
+                                                 stderr=subprocess.PIPE, text=True)))
+    logs, failed = [], []
+    for src, _, pr in procs:
+        out, err = pr.communicate()
+        logs.append(f"==== {src}\n{out}{err}")
+        if pr.returncode != 0:
+            failed.append(f"{src}:\n{err[-3000:]}")
+    (LIBDIR / "ptxas.log").write_text("\n".join(logs))
+    if failed:
+        raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [
-        _nvcc(), ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC",
-        "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v", "--expt-relaxed-constexpr",
-        "-cudart", "static", "-o", str(tmp),
-    ] + [str(CSRC / s) for s in SOURCES]
+    cmd = [nvcc, ARCH, "--shared", "-cudart", "static", "-o", str(tmp)] + [str(o) for _, o, _ in procs]
     proc = subprocess.run(cmd, cwd=str(CSRC), capture_output=True, text=True)
-    (LIBDIR / "ptxas.log").write_text(proc.stdout + proc.stderr)
     if proc.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({proc.returncode}):\n{proc.stderr[-4000:]}")
+        raise RuntimeError(f"nvcc link failed ({proc.returncode}):\n{proc.stderr[-4000:]}")
     if verbose:
-        print(proc.stderr[-2000:])
+        print(logs[0][-2000:])
     os.replace(tmp, LIB)
     return LIB
 

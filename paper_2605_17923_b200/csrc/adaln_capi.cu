@@ -13,6 +13,12 @@
 #include "../../include/adaln_b200.h"
 #include "adaln_kernels.cuh"
 #include "block_kernels.cuh"
+// Parallel build: the kernels are instantiated in instances_{f32,bf16,f16,f64}.cu (one
+// translation unit per dtype, tools/gen_instances.py); this TU only references them.
+// AL_MONOLITHIC (tools/ab_variant.sh) instantiates everything here instead.
+#ifndef AL_MONOLITHIC
+#include "instances_extern.inc"
+#endif
 
 namespace {
 

@@ -11,13 +11,13 @@ mkdir -p "$tmp/p/csrc" "$tmp/include"
 if [ -d "$src" ]; then
   cp -r "$src"/. "$tmp/p/csrc/"; cp "$root/include/adaln_b200.h" "$tmp/include/"
 else
-  for f in adaln_capi.cu adaln_kernels.cuh block_kernels.cuh dtype.cuh ptx.cuh; do
+  for f in adaln_capi.cu adaln_kernels.cuh block_kernels.cuh dtype.cuh ptx.cuh instances_extern.inc; do
     git -C "$root" show "$src:paper_2605_17923_b200/csrc/$f" > "$tmp/p/csrc/$f"; done
   git -C "$root" show "$src:include/adaln_b200.h" > "$tmp/include/adaln_b200.h"
 fi
 mkdir -p "$root/paper_2605_17923_b200/_lib/variants"
 nvcc -gencode=arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --shared -Xcompiler -fPIC \
-  -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -cudart static ${AB_NVCC_FLAGS:-} \
+  -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -cudart static -DAL_MONOLITHIC ${AB_NVCC_FLAGS:-} \
   -o "$root/paper_2605_17923_b200/_lib/variants/$name.so" "$tmp/p/csrc/adaln_capi.cu"
 rm -rf "$tmp"
 echo "built variants/$name.so"
