@@ -308,14 +308,17 @@ def test_deterministic_bitwise(cuda):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("shape,mod", [((1, 8192, 5120), "per_sample"), ((3, 4000, 5120), "per_sample"),
-                                       ((2, 6000, 1536), "per_sample"), ((6000, 2048), "broadcast"),
-                                       ((1, 5000, 4096), "fp32")])
+# the tail is enabled when the last group holds >= 64 rows per CTA (148 CTAs: >= 9 472 rows);
+# (2, 6000, 1536) and (5, 3001, 3072) stay static (fallback path under deterministic=False)
+@pytest.mark.parametrize("shape,mod", [((1, 12000, 5120), "per_sample"), ((3, 10000, 5120), "per_sample"),
+                                       ((2, 6000, 1536), "per_sample"), ((12000, 2048), "broadcast"),
+                                       ((1, 11000, 4096), "fp32"), ((1, 10001, 2048), "fp16"),
+                                       ((2, 10007, 1024), "fp64"), ((5, 3001, 3072), "per_sample")])
 def test_dynamic_tail_backward(shape, mod, cuda):
     """Default (non-deterministic) backward: the dynamic row tail gives dx bit-identical to the
     static partition and dscale/dshift equal to fp32 rounding, every group checked against the
     oracle."""
-    dt = torch.float32 if mod == "fp32" else torch.bfloat16
+    dt = {"fp32": torch.float32, "fp16": torch.float16, "fp64": torch.float64}.get(mod, torch.bfloat16)
     if len(shape) == 2:
         g = torch.Generator().manual_seed(5)
         x = torch.randn(*shape, generator=g).to(dt).to(cuda)
@@ -331,11 +334,22 @@ def test_dynamic_tail_backward(shape, mod, cuda):
         assert torch.equal(got[0], ref[0])
         for u, v in zip(got[1:], ref[1:]):
             assert max_rel_err(f64(u), f64(v)) <= 1e-6
+    # the tail really ran where expected: the last group's column sums come out in another fp32
+    # order (all of thousands of columns agreeing bit for bit by chance is not plausible), while
+    # the static fallback launches the deterministic instance itself
+    b, s_, d = (1, *shape) if len(shape) == 2 else shape
+    code = {torch.float32: nat.AL_F32, torch.bfloat16: nat.AL_BF16, torch.float16: nat.AL_F16,
+            torch.float64: nat.AL_F64}[dt]
+    plan = nat.describe_launch(1, b, s_, d, 0 if len(shape) == 2 else d, code)
+    s_last = b * s_ if len(shape) == 2 else s_
+    dynamic = (plan["path"] == "tma" and plan["rows_per_stage"] in (2, 4)
+               and s_last >= 64 * plan["grid"])
+    assert torch.equal(got[1], ref[1]) != dynamic, plan
     h = lambda t: t.double().cpu().numpy()  # noqa: E731
     if len(shape) == 3:
-        dxo, dsco, dsho = oracle.backward_batched(h(dy), h(x), h(sc), h(mu), h(rs))
+        dxo, dsco, dsho = oracle.backward_batched(h(dy), h(x), h(sc), h(mu), h(rs), threads=8)
     else:
-        dxo, dsco, dsho = oracle.backward_naive(h(dy), h(x), h(sc), h(mu), h(rs))
+        dxo, dsco, dsho = oracle.backward_naive(h(dy), h(x), h(sc), h(mu), h(rs), threads=8)
     assert max_rel_err(h(got[1]), dsco) <= 1e-5
     assert max_rel_err(h(got[2]), dsho) <= 1e-5
     assert max_rel_err(h(got[0]), dxo) <= 2e-2
