@@ -334,6 +334,25 @@ const void* resid_generic_kernel(int dtype) {
 const void* rows16_kernel(int dtype, int vi) {
   return dtype == AL_BF16 ? rows16<__nv_bfloat16>(vi) : rows16<__half>(vi);
 }
+template <typename T>
+const void* rows16r(int vi) {
+  switch (vi) {
+    case 0: return (const void*)al::adaln_fwd_rows16<T, 1, true>;
+    case 1: return (const void*)al::adaln_fwd_rows16<T, 2, true>;
+    case 2: return (const void*)al::adaln_fwd_rows16<T, 3, true>;
+    case 3: return (const void*)al::adaln_fwd_rows16<T, 4, true>;
+    case 4: return (const void*)al::adaln_fwd_rows16<T, 6, true>;
+    case 5: return (const void*)al::adaln_fwd_rows16<T, 8, true>;
+    case 6: return (const void*)al::adaln_fwd_rows16<T, 12, true>;
+    case 7: return (const void*)al::adaln_fwd_rows16<T, 16, true>;
+    case 8: return (const void*)al::adaln_fwd_rows16<T, 20, true>;
+    default: return (const void*)al::adaln_fwd_rows16<T, 24, true>;
+  }
+}
+// gated residual + forward, 16-bit rows: the rows16 kernel's RESID twin
+const void* rows16_resid_kernel(int dtype, int vi) {
+  return dtype == AL_BF16 ? rows16r<__nv_bfloat16>(vi) : rows16r<__half>(vi);
+}
 const void* generic_kernel(int kernel, int dtype) {
   return with_table(dtype, [&](const auto& t) {
     return kernel ? (const void*)t.bwd_generic : (const void*)t.fwd_generic;
@@ -915,6 +934,8 @@ int al_device_init(int device) {
           if (dt == AL_BF16 || dt == AL_F16) {
             rc = ensure_attr(rows16_kernel(dt, vi), device);
             if (rc) return rc;
+            rc = ensure_attr(rows16_resid_kernel(dt, vi), device);
+            if (rc) return rc;
           }
         }
       cudaFuncAttributes fa;
@@ -1008,7 +1029,13 @@ int al_adaln_gate_residual_forward(const void* x, const void* f, const void* gat
     Plan pr;
     pr.path = 2;
     pr.V = kVpl[vi];
-    pr.fn = resid_kernel(dtype, vi);
+    // 16-bit rows of <= 8 vectors per lane (D <= 2 048): the mixed-precision rows16 twin with
+    // the dynamic row tail (pr.R = 2 marks it for enable_dynamic_tail): D = 1 536 5 859 ->
+    // 6 259 GB/s (B = 8, S = 9 450).  Wider rows spill in that kernel (1 KB at D = 5 120:
+    // 3 940 vs 4 949 GB/s), so they and other dtypes take the packed rows kernel's twin.
+    const bool is16 = (dtype == AL_BF16 || dtype == AL_F16) && kVpl[vi] <= 8;
+    pr.fn = is16 ? rows16_resid_kernel(dtype, vi) : resid_kernel(dtype, vi);
+    pr.R = is16 ? 2 : 1;
     pr.threads = 256;
     pr.smem = 3 * static_cast<size_t>(dim) * ct_size(dtype);
     int dev, sms, occ = 0;
@@ -1024,6 +1051,7 @@ int al_adaln_gate_residual_forward(const void* x, const void* f, const void* gat
       p.f = f;
       p.gate = gate;
       p.x_out = x_out;
+      enable_dynamic_tail(pr, p);
       return launch(pr, p, stream, "gate-residual forward launch");
     }
   }

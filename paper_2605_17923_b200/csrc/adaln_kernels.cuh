@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows2(const FwdParams p) {
 // (K - mean)^2 / var, far below the 16-bit inputs' own rounding.  Second pass writes
 // y = (x - mean) * rstd * (1 + scale) + shift.  About 5 instructions per element instead of 8.
 // =====================================================================================
-template <typename T, int VPL>
+template <typename T, int VPL, bool RESID = false>
 __global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
   pdl_enter();
   if (threadIdx.x == 0) AL_TRACE(0, 0);
@@ -588,6 +588,7 @@ __global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   P* s1 = reinterpret_cast<P*>(smem);  // [nvec * NP] : 1 + scale
   P* sh = s1 + p.nvec * NP;            // [nvec * NP] : shift
+  P* gt = sh + p.nvec * NP;            // [nvec * NP] : gate (RESID: the gated-residual twin)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   const int64_t k = blockIdx.x;
@@ -614,6 +615,25 @@ __global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
     for (int i = 0; i < VPL; ++i) {
       const int c = lane + 32 * i;
       v[i] = c < p.nvec ? ld_global_nc_v4(xr + c * 16) : make_uint4(0, 0, 0, 0);
+    }
+    if constexpr (RESID) {
+      // x_out = x + gate * f: one fp32 fma per element, rounded to T (as adaln_fwd_rows<RESID>),
+      // folded into v[] vector by vector while f streams in; the statistics below are then those
+      // of the rounded x_out, so y equals this kernel's forward on x_out bit for bit
+      const uint8_t* fr = static_cast<const uint8_t*>(p.f) + row * RB;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        const bool ok = c < p.nvec;
+        const int cc = ok ? c : 0;
+        const uint4 fw = ok ? ld_global_nc_v4(fr + c * 16) : make_uint4(0, 0, 0, 0);
+        P xa[NP], fa[NP];
+        unpack2<T>(v[i], xa);
+        unpack2<T>(fw, fa);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) xa[e] = fma2(gt[mi(cc, e)], fa[e], xa[e]);
+        v[i] = pack2<T>(xa);
+      }
     }
     P k0[NP];
     unpack2<T>(v[0], k0);
@@ -651,6 +671,7 @@ __global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
         mod_smem(c, a, b);
 #pragma unroll
         for (int e = 0; e < NP; ++e) o[e] = fma2(mul2(sub16x2_f32<T>(w[e], -mean), rs2), a[e], b[e]);
+        if constexpr (RESID) st_global_cs(static_cast<uint8_t*>(p.x_out) + row * RB + c * 16, v[i]);
         st_global_cs(yr + c * 16, pack2<T>(o));
       }
     }
@@ -674,6 +695,15 @@ __global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
         nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y) && finite_ct(b[e].x) && finite_ct(b[e].y));
         s1[mi(c, e)] = add2(a[e], splat2(1.0f));
         sh[mi(c, e)] = b[e];
+      }
+      if constexpr (RESID) {
+        const uint8_t* ga = static_cast<const uint8_t*>(p.gate) + g * p.mod_stride * sizeof(T);
+        unpack2<T>(__ldg(reinterpret_cast<const uint4*>(ga) + c), a);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          nf |= !(finite_ct(a[e].x) && finite_ct(a[e].y));
+          gt[mi(c, e)] = a[e];
+        }
       }
     }
   };

@@ -68,15 +68,18 @@ def test_matches_oracle(dtype, shape, cuda):
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("shape", [(2, 300, 1536), (1, 200, 5120), (2, 9, 12288)])
 def test_y_equals_forward_of_x_out_bitwise(dtype, shape, cuda):
-    """The fused kernel's y/mean/rstd are exactly the one-row-per-warp forward (variant 1)
-    applied to its x_out; rows too wide for it take the unfused composition (residual kernel,
-    then the default forward)."""
+    """The fused kernel's y/mean/rstd are exactly the one-row-per-warp forward applied to its
+    x_out -- the mixed-precision 16-bit kernel (variant 4) for 16-bit rows of <= 8 vectors per
+    lane, the packed rows kernel (variant 1) otherwise; rows too wide for either take the
+    unfused composition (residual kernel, then the default forward)."""
     b, s, d = shape
     x, f, gate, sc, sh = make(b, s, d, dtype, cuda, seed=7)
     xo, y, mu, rs = fused_gate_residual_forward(x, f, gate, sc, sh)
-    rows_kernel = d * x.element_size() // 16 <= 32 * 24
+    nvec = d * x.element_size() // 16
+    rows_kernel = nvec <= 32 * 24
+    variant = 4 if (x.element_size() == 2 and nvec <= 32 * 8) else 1
     try:
-        nat.set_tuning(0, variant=1 if rows_kernel else 0)
+        nat.set_tuning(0, variant=variant if rows_kernel else 0)
         y2, mu2, rs2 = fused_forward(xo, sc, sh)
     finally:
         nat.set_tuning(0)
