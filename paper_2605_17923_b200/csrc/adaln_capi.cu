@@ -687,18 +687,20 @@ al::FwdParams fwd_params(const void* x, const void* scale, const void* shift, vo
 std::atomic<unsigned int> g_sched_seq{0};
 
 unsigned int* sched_slot(int dev) {
-  static unsigned int* base[64] = {};
+  static std::atomic<unsigned int*> base[64] = {};
   if (dev < 0 || dev >= 64) return nullptr;
-  if (base[dev] == nullptr) {
+  unsigned int* b = base[dev].load(std::memory_order_acquire);
+  if (b == nullptr) {
     void* ptr = nullptr;
     if (cudaGetSymbolAddress(&ptr, al::g_sched) != cudaSuccess) {
       (void)cudaGetLastError();
       return nullptr;
     }
-    base[dev] = static_cast<unsigned int*>(ptr);
+    b = static_cast<unsigned int*>(ptr);
+    base[dev].store(b, std::memory_order_release);  // same value from any racing thread
   }
   const unsigned int slot = g_sched_seq.fetch_add(1u) % al::kSchedSlots;
-  return base[dev] + 2 * slot;
+  return b + 2 * slot;
 }
 
 // Fraction of the rows handed out dynamically by the 16-bit rows forward (the rest is a static
