@@ -224,6 +224,13 @@ def run_reference(args, world, rank):
 METRIC = "AdaLN-Modulate fwd+bwd GB/s (% HBM peak), Wan-14B shape; 8-GPU imbalance %"
 
 
+def step_stats(ms: list, nbytes: int, peak: float) -> dict:
+    """Per-launch spread over the timed steps (CUDA events on the launching stream)."""
+    med = statistics.median(ms)
+    return {"median_ms": round(med, 5), "min_ms": round(min(ms), 5), "max_ms": round(max(ms), 5),
+            "median_frac": round(nbytes / (med * 1e-3) / 1e9 / peak, 4)}
+
+
 def imbalance_summary(world: int) -> dict:
     from paper_2605_17923_b200 import sampler as smp
     from paper_2605_17923_b200.catalogs import reference_default_catalog
@@ -268,14 +275,17 @@ def run_ours(args, world, rank, local):
         y, mu, rs = fused_forward(x, sc, sh)
         return fused_backward(dy, x, sc, mu, rs)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
     K = args.steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local, enabled=not args.no_clocks) as clk:
+        # the sampler's first nvidia-smi lines arrive before the GPU work starts; the warm-up
+        # steps then run immediately before the timed region, so the first timed kernel does
+        # not pay the ramp out of an idle power state (a 0.3 s idle gap before a 6 ms timed
+        # region cost the driver's 20-step run +13 us on the average forward in round 1)
         time.sleep(0.3)
+        for _ in range(args.warmup):
+            step()
         barrier(world)
         torch.cuda.synchronize(dev)
         start.record(stream)
@@ -291,6 +301,21 @@ def run_ours(args, world, rank, local):
     elapsed_ms = start.elapsed_time(end)
     fwd_ms = [e[0].elapsed_time(e[1]) for e in ev]
     bwd_ms = [e[1].elapsed_time(e[2]) for e in ev]
+
+    # the reference-facing API's backward (adaln_backward_naive/_dtile force the static,
+    # bit-reproducible partition): timed the same way, after the headline region
+    det_ms = []
+    y, mu, rs = fused_forward(x, sc, sh)
+    for _ in range(args.warmup):
+        fused_backward(dy, x, sc, mu, rs, deterministic=True)
+    torch.cuda.synchronize(dev)
+    dev_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+    for k in range(K):
+        dev_ev[k][0].record(stream)
+        fused_backward(dy, x, sc, mu, rs, deterministic=True)
+        dev_ev[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    det_ms = [e[0].elapsed_time(e[1]) for e in dev_ev]
     elapsed_ms = max_over_ranks(elapsed_ms, world)
     ms_step = elapsed_ms / K
     value = world * nb["total"] / (ms_step * 1e-3) / 1e9
@@ -391,15 +416,26 @@ def run_ours(args, world, rank, local):
                      "unit": "GB/s", "frac": round(bwd_gbs / peak, 4), "traffic": traffic,
                      "bytes_per_launch": nb["bwd"], "avg_ms": round(bwd_avg, 5)},
         "kernels": {"fwd": {"gbs": round(fwd_gbs, 1), "frac": round(fwd_gbs / peak, 4),
-                            "avg_ms": round(fwd_avg, 5), "bytes": nb["fwd"], "plan": fplan},
+                            "avg_ms": round(fwd_avg, 5), **step_stats(fwd_ms, nb["fwd"], peak),
+                            "bytes": nb["fwd"], "plan": fplan},
                     "bwd": {"gbs": round(bwd_gbs, 1), "frac": round(bwd_gbs / peak, 4),
-                            "avg_ms": round(bwd_avg, 5), "bytes": nb["bwd"], "plan": bplan}},
+                            "avg_ms": round(bwd_avg, 5), **step_stats(bwd_ms, nb["bwd"], peak),
+                            "bytes": nb["bwd"], "plan": bplan},
+                    "bwd_deterministic": {
+                        "gbs": round(nb["bwd"] / (sum(det_ms) / K * 1e-3) / 1e9, 1),
+                        "frac": round(nb["bwd"] / (sum(det_ms) / K * 1e-3) / 1e9 / peak, 4),
+                        "avg_ms": round(sum(det_ms) / K, 5), **step_stats(det_ms, nb["bwd"], peak),
+                        "bytes": nb["bwd"],
+                        "what": "fused_backward(deterministic=True): the partition the "
+                                "reference-facing API (adaln_backward_naive/_dtile) runs; "
+                                "dscale/dshift bit-identical run to run",
+                        "plan": bplan}},
         "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "step_ms_min_max": [round(1e3 * min(step_s), 2), round(1e3 * max(step_s), 2)],
                 "path": "adaln_forward + adaln_backward_naive on pinned torch CPU bf16 tensors"},
         "cpu_baseline": cpu,
-        "gpu_launches": 3 * K,
+        "gpu_launches": 3 * K,  # fwd K1 + bwd K2 + K3 per step (the deterministic leg is outside)
         "clocks": clk.summary(),
         "imbalance": imbalance_summary(world),
     }

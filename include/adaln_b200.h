@@ -197,6 +197,12 @@ AL_API int al_set_tuning(int kernel, int vecs_per_thread, int rows_per_stage, in
 AL_API int al_describe_launch(int kernel, int64_t batch, int64_t seq, int64_t dim, int64_t mod_stride,
                        int dtype, int64_t n_tile, int64_t out[7]);
 
+/* Diagnostics: launch one single-thread kernel on `stream` that spins for `spin_ns`
+ * nanoseconds of %globaltimer and writes {globaltimer delta (ns), clock64 delta (SM cycles)}
+ * to the device buffer out[2] -- the SM clock actually running between two hot kernels
+ * (nvidia-smi samples every >= 10 ms and cannot resolve one 0.1 ms launch). */
+AL_API int al_debug_clock_probe(unsigned long long* out, unsigned int spin_ns, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

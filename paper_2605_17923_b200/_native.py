@@ -70,6 +70,7 @@ _SIGNATURES = {
          _i64, _i64, ctypes.c_int, _p, _p],
     ),
     "al_set_tuning": (ctypes.c_int, [ctypes.c_int] * 6),
+    "al_debug_clock_probe": (ctypes.c_int, [_p, ctypes.c_uint, _p]),
     "al_describe_launch": (
         ctypes.c_int,
         [ctypes.c_int, _i64, _i64, _i64, _i64, ctypes.c_int, _i64, ctypes.POINTER(_i64)],
@@ -147,6 +148,11 @@ def set_tuning(kernel: int, vecs_per_thread: int = 0, rows_per_stage: int = 0,
                smem_budget: int = 0, force_generic: bool = False, variant: int = 0) -> None:
     check(load().al_set_tuning(kernel, vecs_per_thread, rows_per_stage, smem_budget,
                                int(force_generic), variant), "al_set_tuning")
+
+
+def clock_probe(out_ptr: int, spin_ns: int, stream_ptr: int) -> None:
+    """Enqueue the SM-clock probe (al_debug_clock_probe) writing 2 uint64 at out_ptr."""
+    check(load().al_debug_clock_probe(out_ptr, spin_ns, stream_ptr), "al_debug_clock_probe")
 
 
 def describe_launch(kernel: int, batch: int, seq: int, dim: int, mod_stride: int, dtype: int,

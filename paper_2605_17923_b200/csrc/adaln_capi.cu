@@ -863,9 +863,28 @@ int gr_plan(int64_t N, int64_t D, int dtype, Plan* out) {
   return AL_OK;
 }
 
+__global__ void clock_probe_kernel(unsigned long long* out, unsigned int spin_ns) {
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  const long long c0 = clock64();
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  } while (t1 - t0 < spin_ns);
+  const long long c1 = clock64();
+  out[0] = t1 - t0;
+  out[1] = static_cast<unsigned long long>(c1 - c0);
+}
+
 }  // namespace
 
 extern "C" {
+
+int al_debug_clock_probe(unsigned long long* out, unsigned int spin_ns, void* stream) {
+  if (!out) return fail(AL_ERR_SHAPE, "null output pointer");
+  clock_probe_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(out, spin_ns);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? AL_OK : cuda_fail(e, "clock probe launch");
+}
 
 int al_abi_version(void) { return 5; }
 
