@@ -203,6 +203,14 @@ AL_API int al_describe_launch(int kernel, int64_t batch, int64_t seq, int64_t di
  * (nvidia-smi samples every >= 10 ms and cannot resolve one 0.1 ms launch). */
 AL_API int al_debug_clock_probe(unsigned long long* out, unsigned int spin_ns, void* stream);
 
+/* Diagnostics: per-launch device timestamps.  While `buf` is set, every al_adaln_forward and
+ * al_adaln_backward launch takes the next pair of buf[capacity][2] (round robin, reset to pair 0
+ * by this call) and writes {earliest CTA start, latest CTA end} (%globaltimer ns; the backward's
+ * end is its stage-2 kernel's) with atomicMin / atomicMax -- the caller initialises the pairs to
+ * {UINT64_MAX, 0}.  Nothing is inserted into the stream, so the kernels' PDL overlap (which an
+ * event record between two launches breaks) is measured as it runs.  NULL disables. */
+AL_API int al_debug_set_timestamps(unsigned long long* buf, int capacity);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,6 +71,7 @@ _SIGNATURES = {
     ),
     "al_set_tuning": (ctypes.c_int, [ctypes.c_int] * 6),
     "al_debug_clock_probe": (ctypes.c_int, [_p, ctypes.c_uint, _p]),
+    "al_debug_set_timestamps": (ctypes.c_int, [_p, ctypes.c_int]),
     "al_describe_launch": (
         ctypes.c_int,
         [ctypes.c_int, _i64, _i64, _i64, _i64, ctypes.c_int, _i64, ctypes.POINTER(_i64)],
@@ -153,6 +154,13 @@ def set_tuning(kernel: int, vecs_per_thread: int = 0, rows_per_stage: int = 0,
 def clock_probe(out_ptr: int, spin_ns: int, stream_ptr: int) -> None:
     """Enqueue the SM-clock probe (al_debug_clock_probe) writing 2 uint64 at out_ptr."""
     check(load().al_debug_clock_probe(out_ptr, spin_ns, stream_ptr), "al_debug_clock_probe")
+
+
+def set_timestamps(buf_ptr: int | None, capacity: int = 0) -> None:
+    """Route per-launch [start, end] device timestamps into a caller-initialised device buffer
+    (al_debug_set_timestamps); None disables."""
+    check(load().al_debug_set_timestamps(buf_ptr, capacity if buf_ptr else 0),
+          "al_debug_set_timestamps")
 
 
 def describe_launch(kernel: int, batch: int, seq: int, dim: int, mod_stride: int, dtype: int,

@@ -86,13 +86,25 @@ def _raise_if_flagged(flag: torch.Tensor | None, what: str) -> None:
         raise NonFiniteInput(f"{what} contains NaN or Inf")
 
 
+def _out_like(t: torch.Tensor | None, shape, dtype, dev, what: str) -> torch.Tensor:
+    """A caller-supplied output (checked) or a fresh one."""
+    if t is None:
+        return torch.empty(shape, dtype=dtype, device=dev)
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != dev or not t.is_contiguous():
+        raise ShapeMismatch(f"{what}: expected contiguous {dtype} {tuple(shape)} on {dev}, "
+                            f"got {t.dtype} {tuple(t.shape)} on {t.device}")
+    return t
+
+
 def fused_forward(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor, eps: float = 1e-6,
                   *, check_finite: bool = False, out: torch.Tensor | None = None,
-                  flag: torch.Tensor | None = None):
+                  flag: torch.Tensor | None = None, out_mean: torch.Tensor | None = None,
+                  out_rstd: torch.Tensor | None = None):
     """y, mean, rstd = AdaLN forward (one HBM pass).  Asynchronous unless check_finite.
 
     ``flag`` (device int32[1]): accumulate the non-finite flag there without synchronising
-    (the caller checks it once, e.g. after a chunked host pipeline)."""
+    (the caller checks it once, e.g. after a chunked host pipeline).  ``out`` / ``out_mean`` /
+    ``out_rstd``: caller-owned outputs (e.g. buffers reused by every step of a captured graph)."""
     if not x.is_cuda:
         raise ShapeMismatch("fused_forward takes CUDA tensors; use adaln_forward for host data")
     if eps <= 0:
@@ -103,10 +115,10 @@ def fused_forward(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor, eps
     x = _prep(x, x.dtype, dev)
     scale = _prep(scale, x.dtype, dev)
     shift = _prep(shift, x.dtype, dev)
-    y = torch.empty_like(x) if out is None else out
+    y = _out_like(out, x.shape, x.dtype, dev, "out")
     sdt = stat_dtype(x.dtype)
-    mean = torch.empty(g.stats_shape, dtype=sdt, device=dev)
-    rstd = torch.empty(g.stats_shape, dtype=sdt, device=dev)
+    mean = _out_like(out_mean, g.stats_shape, sdt, dev, "out_mean")
+    rstd = _out_like(out_rstd, g.stats_shape, sdt, dev, "out_rstd")
     own_flag = check_finite and flag is None
     if own_flag:
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -162,10 +174,21 @@ def fused_gate_residual_forward(x: torch.Tensor, f: torch.Tensor, gate: torch.Te
     return x_out, y, mean, rstd
 
 
+def backward_workspace_bytes(x: torch.Tensor, scale: torch.Tensor, n_tile: int = 0) -> int:
+    """Bytes of scratch fused_backward needs for these shapes (al_adaln_backward_workspace_bytes)."""
+    g = geometry(x, scale)
+    n = nat.load().al_adaln_backward_workspace_bytes(g.batch, g.seq, g.dim, g.mod_stride,
+                                                      dtype_code(x.dtype), n_tile)
+    if n < 0:
+        nat.check(nat.AL_ERR_SHAPE, "al_adaln_backward_workspace_bytes")
+    return max(int(n), 16)
+
+
 def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean: torch.Tensor,
                    rstd: torch.Tensor, *, d_tile: int = 0, n_tile: int = 0,
                    check_finite: bool = False, flag: torch.Tensor | None = None,
-                   deterministic: bool | None = None):
+                   deterministic: bool | None = None, out: tuple | None = None,
+                   workspace: torch.Tensor | None = None):
     """dx, dscale, dshift in one pass over (dy, x) + a fixed-order cross-CTA reduction.
 
     deterministic: True keeps the static row partition (dscale/dshift bit-identical run to
@@ -173,6 +196,8 @@ def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean:
     whichever SM is free (faster: HBM bandwidth is not shared evenly between SMs), which moves
     the last group's dscale/dshift at fp32 rounding level from run to run -- dx is identical
     either way.  None (default) follows ``torch.are_deterministic_algorithms_enabled()``.
+    ``out`` = (dx, dscale, dshift) and ``workspace`` (uint8, at least
+    ``al_adaln_backward_workspace_bytes``): caller-owned buffers, e.g. reused by a captured graph.
     """
     if deterministic is None:
         deterministic = torch.are_deterministic_algorithms_enabled()
@@ -195,10 +220,17 @@ def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean:
                                                      n_tile)
     if ws_bytes < 0:
         nat.check(nat.AL_ERR_SHAPE, "al_adaln_backward_workspace_bytes")
-    ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
-    dx = torch.empty_like(x)
-    dscale = torch.empty(g.grad_shape, dtype=sdt, device=dev)
-    dshift = torch.empty(g.grad_shape, dtype=sdt, device=dev)
+    if workspace is None:
+        ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
+    else:
+        if workspace.device != dev or workspace.dtype != torch.uint8 or workspace.numel() < ws_bytes:
+            raise ShapeMismatch(f"workspace: need >= {ws_bytes} uint8 bytes on {dev}")
+        ws = workspace
+        ws_bytes = workspace.numel()
+    o = out if out is not None else (None, None, None)
+    dx = _out_like(o[0], x.shape, x.dtype, dev, "out[0] (dx)")
+    dscale = _out_like(o[1], g.grad_shape, sdt, dev, "out[1] (dscale)")
+    dshift = _out_like(o[2], g.grad_shape, sdt, dev, "out[2] (dshift)")
     own_flag = check_finite and flag is None
     if own_flag:
         flag = torch.zeros(1, dtype=torch.int32, device=dev)

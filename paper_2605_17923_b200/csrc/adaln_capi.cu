@@ -211,6 +211,25 @@ const void* tma_dyn_kernel(int dtype, int V, int R, bool full) {
     return full ? (const void*)t.bwd_dyn_full[a][b] : (const void*)t.bwd_dyn[a][b];
   });
 }
+// skewed-pipeline backward (adaln_bwd_pipe): bf16/fp16, V in {1, 2, 4}, R in {1, 2}
+template <typename T, int V>
+const void* pipe_t(int R, bool full, bool dyn) {
+  if (R == 1) {
+    if (full) return dyn ? (const void*)al::adaln_bwd_pipe<T, V, 1, true, true>
+                         : (const void*)al::adaln_bwd_pipe<T, V, 1, true, false>;
+    return dyn ? (const void*)al::adaln_bwd_pipe<T, V, 1, false, true>
+               : (const void*)al::adaln_bwd_pipe<T, V, 1, false, false>;
+  }
+  if (full) return dyn ? (const void*)al::adaln_bwd_pipe<T, V, 2, true, true>
+                       : (const void*)al::adaln_bwd_pipe<T, V, 2, true, false>;
+  return dyn ? (const void*)al::adaln_bwd_pipe<T, V, 2, false, true>
+             : (const void*)al::adaln_bwd_pipe<T, V, 2, false, false>;
+}
+const void* pipe_kernel(int dtype, int V, int R, bool full, bool dyn) {
+  if (V != 2 || (R != 1 && R != 2)) return nullptr;
+  if (dtype == AL_BF16) return pipe_t<__nv_bfloat16, 2>(R, full, dyn);
+  return nullptr;
+}
 const void* rows_kernel(int dtype, int vi, bool repack) {
   return with_table(dtype, [&](const auto& t) {
     return repack ? (const void*)t.rows_rp[vi] : (const void*)t.rows[vi];
@@ -676,7 +695,22 @@ al::FwdParams fwd_params(const void* x, const void* scale, const void* shift, vo
   p.x_out = nullptr;
   p.sched = nullptr;
   p.N_static = N;
+  p.ts = nullptr;
   return p;
+}
+
+// ---------------------------------------------------------------- launch timestamps
+// al_debug_set_timestamps: every al_adaln_forward / al_adaln_backward launch takes the next
+// [start, end] pair of the caller's device buffer (round robin over `capacity` pairs).
+std::atomic<unsigned long long*> g_ts_buf{nullptr};
+std::atomic<int> g_ts_cap{0};
+std::atomic<unsigned int> g_ts_next{0};
+
+unsigned long long* next_ts() {
+  unsigned long long* b = g_ts_buf.load(std::memory_order_acquire);
+  const int cap = g_ts_cap.load(std::memory_order_acquire);
+  if (b == nullptr || cap <= 0) return nullptr;
+  return b + 2 * static_cast<size_t>(g_ts_next.fetch_add(1u) % static_cast<unsigned int>(cap));
 }
 
 // ---------------------------------------------------------------- dynamic row tail
@@ -879,6 +913,15 @@ __global__ void clock_probe_kernel(unsigned long long* out, unsigned int spin_ns
 
 extern "C" {
 
+int al_debug_set_timestamps(unsigned long long* buf, int capacity) {
+  if (buf != nullptr && capacity <= 0) return fail(AL_ERR_VALUE, "capacity must be positive");
+  g_ts_buf.store(nullptr, std::memory_order_release);
+  g_ts_cap.store(buf ? capacity : 0, std::memory_order_release);
+  g_ts_next.store(0u);
+  g_ts_buf.store(buf, std::memory_order_release);
+  return AL_OK;
+}
+
 int al_debug_clock_probe(unsigned long long* out, unsigned int spin_ns, void* stream) {
   if (!out) return fail(AL_ERR_SHAPE, "null output pointer");
   clock_probe_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(out, spin_ns);
@@ -1021,6 +1064,7 @@ int al_adaln_forward(const void* x, const void* scale, const void* shift, void* 
   if (rc) return rc;
   al::FwdParams p = fwd_params(x, scale, shift, y, mean, rstd, seq, N, dim, mod_stride, dtype,
                                eps, nonfinite, pl);
+  p.ts = next_ts();
   enable_dynamic_tail(pl, p);
   return launch(pl, p, stream, "forward launch");
 }
@@ -1196,6 +1240,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   p.sched = nullptr;
   p.N_static = N;
   p.tail_slot0 = -1;
+  p.ts = next_ts();
   if (n_dyn) {
     int dev;
     const bool full = pl.threads - 32 == p.nvec / pl.V && p.nvec % pl.V == 0;
@@ -1208,6 +1253,32 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
       p.sched = slot;
       p.N_static = N - n_dyn;
       p.tail_slot0 = nslots_static;
+    }
+  }
+  // Skewed-pipeline stage 1 (variant 3 while under evaluation): same ring/slot contract, its
+  // own ring depth (the consumers hold two slots at a time)
+  if (pl.path == 1 && tu.variant == 3) {
+    const int R = tu.R ? tu.R : 2;
+    const bool full = pl.threads - 32 == p.nvec / pl.V && p.nvec % pl.V == 0;
+    const void* fn = pipe_kernel(dtype, pl.V, R, full, p.sched != nullptr);
+    if (fn != nullptr && (R == 1 || R == 2)) {
+      const int ncw = (pl.threads - 32) / 32;
+      const size_t stage = 2 * static_cast<size_t>(R) * p.row_bytes;
+      auto extra = [&](int ns) {
+        return static_cast<size_t>(2 * ns + 4) * 8 + 4 * ncw * 2 * R * cs + 16 +
+               static_cast<size_t>(ns) * (8 + 4 + 2 * R * cs) + 32;
+      };
+      const size_t budget = tu.smem_budget ? static_cast<size_t>(tu.smem_budget) : 210 * 1024;
+      int ns = 2;
+      while (ns < 12 && (ns + 1) * stage + extra(ns + 1) <= budget) ++ns;
+      int dev;
+      if (ns >= 3 && cudaGetDevice(&dev) == cudaSuccess && ensure_attr(fn, dev) == AL_OK) {
+        pl.fn = fn;
+        pl.NS = ns;
+        pl.R = R;
+        pl.smem = ns * stage + extra(ns);
+        p.nstages = ns;
+      }
     }
   }
   // Fused stage 2: the TMA kernel reduces the partials itself behind a grid barrier, which
@@ -1231,12 +1302,12 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   // stage 2: 16-byte vector form when every partial row is 16-byte aligned
   const void* rk = reduce_kernel(dtype, vec);
   int64_t G64 = pl.grid;
-  void* rargs[] = {&workspace, &dscale, &dshift, &p.N,      &p.S_grp,
-                   &p.D,       &G64,    &p.nslots, &p.N_static, &p.tail_slot0};
-  const int64_t cols_per_cta = vec ? 16 * (16 / cs) : 32;
+  void* rargs[] = {&workspace, &dscale, &dshift,     &p.N,           &p.S_grp, &p.D,
+                   &G64,       &p.nslots, &p.N_static, &p.tail_slot0, &p.ts};
+  const int64_t cols_per_cta = vec ? al::kRedCV * (16 / cs) : 32;
   dim3 rgrid(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
              static_cast<unsigned>(ngroups));
-  e = launch_k(rk, rgrid, dim3(1024), rargs, 0, st, kPdlBwd2);
+  e = launch_k(rk, rgrid, dim3(vec ? 512 : 1024), rargs, 0, st, kPdlBwd2);
   if (e != cudaSuccess) return cuda_fail(e, "backward stage-2 launch");
   return AL_OK;
 }
@@ -1341,10 +1412,11 @@ int al_qk_rmsnorm_backward(const void* qkv, int64_t row_stride, const void* wq, 
   const void* rk = reduce_kernel(dtype, true);
   int64_t N64 = n_rows, S64 = n_rows, D64 = dim, G64 = pl.grid, ns = pl.grid;
   int64_t tail0 = -1;
-  void* rargs[] = {&workspace, &dwq, &dwk, &N64, &S64, &D64, &G64, &ns, &N64, &tail0};
-  const int64_t cols_per_cta = 16 * (16 / cs);
+  unsigned long long* no_ts = nullptr;
+  void* rargs[] = {&workspace, &dwq, &dwk, &N64, &S64, &D64, &G64, &ns, &N64, &tail0, &no_ts};
+  const int64_t cols_per_cta = al::kRedCV * (16 / cs);
   e = launch_k(rk, dim3(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta), 1),
-               dim3(1024), rargs, 0, st, kPdlBwd2);
+               dim3(512), rargs, 0, st, kPdlBwd2);
   if (e != cudaSuccess) return cuda_fail(e, "qk-norm backward stage-2 launch");
   return AL_OK;
 }
@@ -1412,11 +1484,12 @@ int al_gate_residual_backward(const void* dxn, const void* gxo, const void* f, c
   void* none = nullptr;
   int64_t G64 = pl.grid, D64 = dim, N64 = N, S64 = p.S_grp, ns = nslots;
   int64_t tail0 = -1;
-  void* rargs[] = {&workspace, &dgate, &none, &N64, &S64, &D64, &G64, &ns, &N64, &tail0};
-  const int64_t cols_per_cta = 16 * (16 / cs);
+  unsigned long long* no_ts = nullptr;
+  void* rargs[] = {&workspace, &dgate, &none, &N64, &S64, &D64, &G64, &ns, &N64, &tail0, &no_ts};
+  const int64_t cols_per_cta = al::kRedCV * (16 / cs);
   e = launch_k(rk, dim3(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
                         static_cast<unsigned>(ngroups)),
-               dim3(1024), rargs, 0, st, kPdlBwd2);
+               dim3(512), rargs, 0, st, kPdlBwd2);
   if (e != cudaSuccess) return cuda_fail(e, "gated-residual backward stage-2 launch");
   return AL_OK;
 }

@@ -60,6 +60,7 @@ struct FwdParams {
   // (N_static == N).
   unsigned int* sched;
   int64_t N_static;
+  unsigned long long* ts;  // nullable: per-launch device timestamps (ptx.cuh ts_begin/ts_end)
 };
 
 // Ticket-counter slots for dynamically scheduled launches; the host hands launches slots
@@ -96,6 +97,7 @@ struct BwdParams {
   unsigned int* sched;
   int64_t N_static;
   int64_t tail_slot0;
+  unsigned long long* ts;  // nullable: start stamped here, end by the stage-2 kernel
 };
 
 // Row partition shared by stage 1 and stage 2.
@@ -159,6 +161,7 @@ template <typename T, int VPL, bool PACKED, bool PREFETCH = false, bool STAGED =
           bool RESID = false>
 __global__ void __launch_bounds__(STAGED ? 512 : 256, RESID ? 2 : 0) adaln_fwd_rows(const FwdParams p) {
   pdl_enter();
+  ts_begin(p.ts);
   static_assert(!(RESID && STAGED), "the gated residual is not staged");
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
@@ -574,6 +577,7 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows2(const FwdParams p) {
 template <typename T, int VPL, bool RESID = false>
 __global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
   pdl_enter();
+  ts_begin(p.ts);
   if (threadIdx.x == 0) AL_TRACE(0, 0);
   static_assert(sizeof(T) == 2, "16-bit rows only");
   using P = float2;
@@ -758,6 +762,10 @@ __global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
   if (tid == 0) AL_TRACE(0, 1);
 #endif
   if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+  if (p.ts != nullptr) {
+    __syncthreads();
+    if (tid == 0) ts_end(p.ts);
+  }
 }
 
 // =====================================================================================
@@ -1304,6 +1312,7 @@ __device__ void fused_stage2(const BwdParams& p, int nc, int tid) {
 template <typename T, int V, int R, bool FULL, bool DYN>
 __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdParams p) {
   pdl_enter();
+  ts_begin(p.ts);
   if (threadIdx.x == 0) AL_TRACE(1, 0);
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
@@ -1812,24 +1821,425 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
 }
 
 // =====================================================================================
-// Backward stage 2: dscale/dshift[g, d] = sum over the CTAs covering group g, ascending.
-// Vector form (D a multiple of 16 B of partials): block = 1024 threads = 16 column vectors
-// (64 fp32 / 32 fp64 columns) x 64 slot lanes; each thread issues all of its 16-byte loads
-// before adding, the two half-warps of a warp are combined by a shuffle and the 32 warps in
-// ascending order through shared memory -- a fixed order, so the result is deterministic.
+// Backward stage 1, skewed-pipeline TMA path (K2p).  Same ring, producer and column-owner
+// layout as adaln_bwd_tma, but no per-stage lock step: a consumer warp runs phase 1 of stage i
+// (row sums of g and g*xhat, column accumulators), deposits its row-sum partials in a small
+// reduction ring and ARRIVES on that entry's mbarrier (no bar.sync), then runs phase 2 of stage
+// i-1 -- whose cross-warp totals were completed by every warp's phase 1 of i-1 while this warp
+// was busy -- re-reading x and dy of stage i-1 from the still-held ring slot (xhat and g are
+// recomputed, not kept in registers across the barrier), writes dx and releases the slot.
+// The barrier latency is thereby overlapped with the next stage's phase 1, warps drift freely
+// instead of bursting the FMA pipe in lock step, and the ~64 registers that held xhat and g are
+// gone (97 instead of 168 per thread).
+// Invariants: a warp in phase 1 of stage i has finished phase 2 of i-2, which needed every warp's
+// phase 1 of i-2, so at most three reduction entries (i-2, i-1, i) are live: KR = 4 entries.
+// (1 + scale) is group-constant; a group change drains the pending stage first, so phase 2 always
+// sees the modulation its stage was accumulated with.
 // =====================================================================================
+template <typename T, int V, int R, bool FULL, bool DYN>
+__global__ void __launch_bounds__(384, 1) adaln_bwd_pipe(const BwdParams p) {
+  pdl_enter();
+  ts_begin(p.ts);
+  if (threadIdx.x == 0) AL_TRACE(1, 0);
+  using CT = typename Traits<T>::CT;
+  using P = typename PairOf<CT>::type;
+  constexpr int EPV = Traits<T>::EPV;
+  constexpr int NP = EPV / 2;
+  constexpr int KR = 4;       // reduction-ring entries
+  constexpr int NV = 2 * R;   // row-sum values per stage (sum g, sum g*xhat per row)
+  constexpr int GRP = 32 / NV;
+  extern __shared__ __align__(128) uint8_t smem[];
+
+  const int nc = blockDim.x - 32;
+  const int ncw = nc >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NS = p.nstages;
+  const int RB = p.row_bytes;
+  const int stage_bytes = 2 * R * RB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(NS) * stage_bytes);
+  uint64_t* empty = full + NS;
+  uint64_t* rbar = empty + NS;                        // [KR]: row-sum entry complete
+  CT* red = reinterpret_cast<CT*>(rbar + KR);         // [KR][ncw][NV]
+  int64_t* h_row = reinterpret_cast<int64_t*>(
+      (reinterpret_cast<uintptr_t>(red + KR * ncw * NV) + 7) & ~uintptr_t(7));
+  int* h_n = reinterpret_cast<int*>(h_row + NS);
+  CT* h_m = reinterpret_cast<CT*>((reinterpret_cast<uintptr_t>(h_n + NS) + 7) & ~uintptr_t(7));
+  CT* h_r = h_m + NS * R;
+
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N_static, p.G), r1 = part_begin(k + 1, p.N_static, p.G);
+  const bool dyn = DYN && p.sched != nullptr;
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ncw);
+    }
+    for (int b = 0; b < KR; ++b) mbar_init(&rbar[b], ncw * NV);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == ncw) {  // ---------------- producer (as adaln_bwd_tma) ----------------
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const uint8_t* xb = static_cast<const uint8_t*>(p.x);
+      const uint8_t* db = static_cast<const uint8_t*>(p.dy);
+      StageWalker w;
+      w.init(r0, r1, p.S_grp);
+      int s = 0;
+      uint32_t f = 0;
+      auto issue = [&](int64_t start, int rows) {
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(2 * rows * RB));
+        uint8_t* dst = smem + static_cast<size_t>(s) * stage_bytes;
+        for (int rr = 0; rr < rows; ++rr) {
+          bulk_g2s(dst + rr * RB, xb + (start + rr) * RB, RB, &full[s], pol);
+          bulk_g2s(dst + (R + rr) * RB, db + (start + rr) * RB, RB, &full[s], pol);
+        }
+        if (++s == NS) {
+          s = 0;
+          ++f;
+        }
+      };
+      while (!w.done()) {
+        int64_t start, g;
+        const int rows = w.next(R, start, g);
+        if (f > 0) mbar_wait(&empty[s], (f - 1) & 1);
+        issue(start, rows);
+      }
+      if (dyn) {
+        const CT* mean_p = static_cast<const CT*>(p.mean);
+        const CT* rstd_p = static_cast<const CT*>(p.rstd);
+        auto stats = [&](int64_t start, CT* m, CT* r) {
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const bool ok = start + rr < p.N;
+            m[rr] = ok ? mean_p[start + rr] : CT(0);
+            r[rr] = ok ? rstd_p[start + rr] : CT(0);
+          }
+        };
+        int64_t start = p.N_static + static_cast<int64_t>(atomicAdd(p.sched, 1u)) * R;
+        CT m[R], r[R];
+        stats(start, m, r);
+        unsigned int tn = atomicAdd(p.sched, 1u);
+        while (true) {
+          const int rows = start < p.N ? static_cast<int>(p.N - start < R ? p.N - start : R) : 0;
+          if (f > 0) mbar_wait(&empty[s], (f - 1) & 1);
+          h_row[s] = start;
+          h_n[s] = rows;
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            h_m[s * R + rr] = m[rr];
+            h_r[s * R + rr] = r[rr];
+          }
+          if (rows == 0) {
+            mbar_arrive(&full[s]);
+            break;
+          }
+          issue(start, rows);
+          start = p.N_static + static_cast<int64_t>(tn) * R;
+          if (start < p.N) {
+            stats(start, m, r);
+            tn = atomicAdd(p.sched, 1u);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  uint32_t vmask = FULL ? (1u << V) - 1 : 0u;
+  int coff[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    coff[j] = (tid + j * nc) * 16;
+    if (!FULL && tid + j * nc < p.nvec) vmask |= 1u << j;
+  }
+  const CT invD = CT(1) / static_cast<CT>(p.D);
+  const CT* mean_p = static_cast<const CT*>(p.mean);
+  const CT* rstd_p = static_cast<const CT*>(p.rstd);
+  CT* ws_sc = static_cast<CT*>(p.ws);
+  CT* ws_sh = ws_sc + p.nslots * p.D;
+  bool nf = false;
+  const uint32_t smem_u = smem_addr(smem);
+
+  P s1[V][NP], acc_sc[V][NP], acc_sh[V][NP];
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+#pragma unroll
+    for (int e = 0; e < NP; ++e) acc_sc[j][e] = acc_sh[j][e] = splat2(CT(0));
+
+  auto flush = [&](int64_t slot) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (vmask >> j & 1) {
+        const int64_t col = static_cast<int64_t>(coff[j] / 16) * EPV;
+        P* a = reinterpret_cast<P*>(ws_sc + slot * p.D + col);
+        P* b = reinterpret_cast<P*>(ws_sh + slot * p.D + col);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          a[e] = acc_sc[j][e];
+          b[e] = acc_sh[j][e];
+          acc_sc[j][e] = acc_sh[j][e] = splat2(CT(0));
+        }
+      }
+    }
+  };
+  auto load_scale = [&](int64_t g) {
+    const uint8_t* sc = static_cast<const uint8_t*>(p.scale) + g * p.mod_stride * sizeof(T);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (vmask >> j & 1) {
+        unpack2<T>(__ldg(reinterpret_cast<const uint4*>(sc + coff[j])), s1[j]);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) s1[j][e] = add2(s1[j][e], splat2(CT(1)));
+      } else {
+#pragma unroll
+        for (int e = 0; e < NP; ++e) s1[j][e] = splat2(CT(0));
+      }
+    }
+  };
+
+  // ring cursor (consumer side) and reduction-ring counter
+  int s = 0;
+  uint32_t ph = 0;
+  uint32_t it = 0;
+  // the stage whose phase 2 is pending
+  struct Pend {
+    int64_t rb;
+    int rows, slot;
+    uint32_t it;
+    CT m[R], r[R];
+  } pd;
+  bool pending = false;
+
+  // phase 1 of the stage in ring slot s (the caller has waited on full[s])
+  auto phase1 = [&](auto all_tag, int rows, const CT* mc, const CT* rc) {
+    constexpr bool ALL = decltype(all_tag)::value;
+    const uint32_t stx_u = smem_u + static_cast<uint32_t>(s * stage_bytes);
+    const uint32_t std_u = stx_u + static_cast<uint32_t>(R * RB);
+    CT rowsum[NV];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const bool live = ALL || rr < rows;
+      const P nm = splat2(-mc[rr]), r2 = splat2(rc[rr]);
+      const P nmr = splat2(-mc[rr] * rc[rr]);
+      P sg[2] = {splat2(CT(0)), splat2(CT(0))}, sgx[2] = {splat2(CT(0)), splat2(CT(0))};
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const bool ok = live && (vmask >> j & 1);
+        P xv[NP], dv[NP];
+        const uint32_t o = static_cast<uint32_t>(rr * RB + coff[j]);
+        unpack2<T>(ok ? ld_shared_v4_u32(stx_u + o) : make_uint4(0, 0, 0, 0), xv);
+        unpack2<T>(ok ? ld_shared_v4_u32(std_u + o) : make_uint4(0, 0, 0, 0), dv);
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          P xh;
+          if constexpr (sizeof(T) == 2) xh = fma2(xv[e], r2, nmr);
+          else xh = mul2(add2(xv[e], nm), r2);
+          const P gg = mul2(dv[e], s1[j][e]);
+          sg[e & 1] = add2(sg[e & 1], gg);
+          sgx[e & 1] = fma2(gg, xh, sgx[e & 1]);
+          acc_sh[j][e] = add2(acc_sh[j][e], dv[e]);
+          acc_sc[j][e] = fma2(dv[e], xh, acc_sc[j][e]);
+        }
+      }
+      const P tsg = add2(sg[0], sg[1]), tsgx = add2(sgx[0], sgx[1]);
+      rowsum[2 * rr] = tsg.x + tsg.y;
+      rowsum[2 * rr + 1] = tsgx.x + tsgx.y;
+    }
+    const int b = static_cast<int>(it % KR);
+    const CT u = warp_reduce_scatter<NV>(rowsum, lane);
+    if ((lane & (GRP - 1)) == 0) {
+      red[(b * ncw + warp) * NV + lane / GRP] = u;
+      mbar_arrive(&rbar[b]);  // release: the entry write above is visible to the waiters
+    }
+  };
+
+  // phase 2 of the pending stage: totals, dx from the re-read slot, slot release
+  auto phase2 = [&](auto all_tag) {
+    constexpr bool ALL = decltype(all_tag)::value;
+    const int b = static_cast<int>(pd.it % KR);
+    mbar_wait(&rbar[b], (pd.it / KR) & 1);
+    CT tot[NV];
+    {
+      const CT* rd = red + b * ncw * NV;
+      const int nval = ncw * NV;
+      CT s_l = CT(0);
+      for (int i = lane; i < nval; i += 32) s_l += rd[i];
+#pragma unroll
+      for (int off = NV; off < 32; off <<= 1) s_l += __shfl_xor_sync(0xffffffffu, s_l, off);
+#pragma unroll
+      for (int q = 0; q < NV; ++q) tot[q] = __shfl_sync(0xffffffffu, s_l, q);
+    }
+    const uint32_t stx_u = smem_u + static_cast<uint32_t>(pd.slot * stage_bytes);
+    const uint32_t std_u = stx_u + static_cast<uint32_t>(R * RB);
+    uint8_t* dxrow = static_cast<uint8_t*>(p.dx) + pd.rb * RB;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (ALL || rr < pd.rows) {
+        const CT rr_ = pd.r[rr];
+        const CT c0 = -rr_ * tot[2 * rr] * invD, c1 = -rr_ * tot[2 * rr + 1] * invD;
+        const P r2 = splat2(rr_);
+        // 16-bit: dx = g*r + (x*(c1*r) + (c0 - c1*m*r)), xhat folded into the constants;
+        // 32/64-bit: xhat recomputed exactly as in phase 1, dx = g*r + (xhat*c1 + c0)
+        const P a1 = splat2(c1 * rr_), a0 = splat2(c0 - c1 * pd.m[rr] * rr_);
+        const P nm = splat2(-pd.m[rr]), pc1 = splat2(c1), pc0 = splat2(c0);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if (vmask >> j & 1) {
+            P xv[NP], dv[NP], o[NP];
+            const uint32_t off = static_cast<uint32_t>(rr * RB + coff[j]);
+            unpack2<T>(ld_shared_v4_u32(stx_u + off), xv);
+            unpack2<T>(ld_shared_v4_u32(std_u + off), dv);
+#pragma unroll
+            for (int e = 0; e < NP; ++e) {
+              const P gg = mul2(dv[e], s1[j][e]);
+              if constexpr (sizeof(T) == 2) {
+                o[e] = fma2(gg, r2, fma2(xv[e], a1, a0));
+              } else {
+                const P xh = mul2(add2(xv[e], nm), r2);
+                o[e] = fma2(gg, r2, fma2(xh, pc1, pc0));
+              }
+            }
+            st_global_cs(dxrow + rr * RB + coff[j], pack2<T>(o));
+          }
+        }
+        if (tid == 0) nf |= !(finite_ct(tot[2 * rr]) && finite_ct(tot[2 * rr + 1]));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[pd.slot]);
+    pending = false;
+  };
+  auto drain = [&]() {
+    if (pending) {
+      if (pd.rows == R) phase2(std::true_type{});
+      else phase2(std::false_type{});
+    }
+  };
+  // one stage: phase 1 of it, then phase 2 of the previous one
+  auto step = [&](int64_t rb, int rows, const CT* mc, const CT* rc) {
+    if (rows == R) phase1(std::true_type{}, rows, mc, rc);
+    else phase1(std::false_type{}, rows, mc, rc);
+    drain();
+    pd.rb = rb;
+    pd.rows = rows;
+    pd.slot = s;
+    pd.it = it;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      pd.m[rr] = mc[rr];
+      pd.r[rr] = rc[rr];
+    }
+    pending = true;
+    ++it;
+    if (++s == NS) {
+      s = 0;
+      ph ^= 1;
+    }
+  };
+
+  // static head: the producer's StageWalker sequence, segment by segment
+  int64_t row = r0;
+  while (row < r1) {
+    const int64_t g = row / p.S_grp;
+    const int64_t seg_end = min((g + 1) * p.S_grp, r1);
+    const int n = static_cast<int>(seg_end - row);
+    drain();  // phase 2 of the previous group's last stage needs that group's (1 + scale)
+    load_scale(g);
+    const CT* mp = mean_p + row;
+    const CT* rp = rstd_p + row;
+    CT mc[R], rc[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      mc[rr] = rr < n ? mp[rr] : CT(0);
+      rc[rr] = rr < n ? rp[rr] : CT(0);
+    }
+    for (int i = 0; i * R < n; ++i) {
+      const int rows = n - i * R < R ? n - i * R : R;
+      CT mn[R], rn[R];
+      const int nx = (i + 1) * R, left = n - nx;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        mn[rr] = rr < left ? mp[nx + rr] : CT(0);
+        rn[rr] = rr < left ? rp[nx + rr] : CT(0);
+      }
+      mbar_wait(&full[s], ph);
+      step(row + i * R, rows, mc, rc);
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        mc[rr] = mn[rr];
+        rc[rr] = rn[rr];
+      }
+    }
+    flush(k + g);  // accumulators are phase-1 state: the pending phase 2 does not touch them
+    row = seg_end;
+  }
+
+  if (dyn) {
+    drain();
+    load_scale((p.N - 1) / p.S_grp);
+    while (true) {
+      mbar_wait(&full[s], ph);
+      const int64_t rb = h_row[s];
+      const int rows = h_n[s];
+      if (rows == 0) break;
+      CT mc[R], rc[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        mc[rr] = h_m[s * R + rr];
+        rc[rr] = h_r[s * R + rr];
+      }
+      step(rb, rows, mc, rc);
+    }
+    flush(p.tail_slot0 + k);
+  }
+  drain();
+#ifdef AL_CTA_TRACE
+  named_bar_sync(1, nc);
+  if (tid == 0) AL_TRACE(1, 1);
+#endif
+  if (nf && p.nonfinite) atomicExch(p.nonfinite, 1);
+  if (dyn) {
+    named_bar_sync(1, nc);
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(p.sched + 1, 1u) == static_cast<unsigned int>(p.G - 1)) {
+        atomicExch(p.sched, 0u);
+        atomicExch(p.sched + 1, 0u);
+      }
+    }
+  }
+}
+
+// =====================================================================================
+// Backward stage 2: dscale/dshift[g, d] = sum over the CTAs covering group g, ascending.
+// Vector form (D a multiple of 16 B of partials): block = 512 threads = kRedCV column vectors
+// (8 x 16 B = 32 fp32 / 16 fp64 columns) x 64 slot lanes, 2 CTAs per SM, so a cfg2 reduction
+// (296 slots, 160 CTAs) is one wave with <= 5 slots per thread, all loads of a thread in flight
+// before the first add (the kernel is a latency chain, not a bandwidth one).  Slot lanes are
+// combined by a fixed shuffle tree inside the warp and the 16 warps in ascending order through
+// shared memory -- a fixed order, so the result is deterministic.
+// =====================================================================================
+constexpr int kRedCV = 8;  // 16-byte column vectors per stage-2 CTA
 template <typename CT>
-__global__ void __launch_bounds__(1024) adaln_bwd_reduce_vec(const CT* __restrict__ ws,
+__global__ void __launch_bounds__(512, 2) adaln_bwd_reduce_vec(const CT* __restrict__ ws,
                                                              CT* __restrict__ dscale,
                                                              CT* __restrict__ dshift, int64_t N,
                                                              int64_t S_grp, int64_t D, int64_t G,
                                                              int64_t nslots, int64_t Ns,
-                                                             int64_t tail0) {
-  pdl_enter();
-  constexpr int VE = 16 / sizeof(CT);  // columns per 16-byte vector
-  constexpr int COLS = 16 * VE;        // columns per CTA
-  __shared__ double part[2][32][COLS + 1];
-  const int t = threadIdx.x, hl = t & 15, sl = t >> 4, warp = t >> 5;
+                                                             int64_t tail0,
+                                                             unsigned long long* ts) {
+  pdl_wait();
+  constexpr int VE = 16 / sizeof(CT);   // columns per 16-byte vector
+  constexpr int CV = kRedCV;
+  constexpr int COLS = CV * VE;         // columns per CTA
+  constexpr int SL = 512 / CV;          // slot lanes
+  constexpr int NW = 512 / 32;          // warps
+  __shared__ double part[2][NW][COLS + 1];
+  const int t = threadIdx.x, hl = t % CV, sl = t / CV, warp = t >> 5;
   const int64_t g = blockIdx.y;
   const int64_t col = static_cast<int64_t>(blockIdx.x) * COLS + hl * VE;
   // slots of group g: the static owners of its rows below Ns (slot k + g, ascending k), then --
@@ -1855,12 +2265,12 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce_vec(const CT* __restric
     const int64_t jump = tail0 - (kf + g) - n1;
     auto off = [&](int64_t i) { return (i < n1 ? i : i + jump) * D; };
     int64_t i = sl;
-    for (; i + 192 < n; i += 256) {  // 4 slots x 2 arrays of 16-byte loads in flight
+    for (; i + 3 * SL < n; i += 4 * SL) {  // 4 slots x 2 arrays of 16-byte loads in flight
       uint4 va[4], vb[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        va[u] = __ldg(reinterpret_cast<const uint4*>(sc + off(i + 64 * u)));
-        vb[u] = __ldg(reinterpret_cast<const uint4*>(sh + off(i + 64 * u)));
+        va[u] = __ldcg(reinterpret_cast<const uint4*>(sc + off(i + SL * u)));
+        vb[u] = __ldcg(reinterpret_cast<const uint4*>(sh + off(i + SL * u)));
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -1873,38 +2283,58 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce_vec(const CT* __restric
         }
       }
     }
-    for (; i < n; i += 64) {
-      const uint4 va = __ldg(reinterpret_cast<const uint4*>(sc + off(i)));
-      const uint4 vb = __ldg(reinterpret_cast<const uint4*>(sh + off(i)));
-      const CT* pa = reinterpret_cast<const CT*>(&va);
-      const CT* pb = reinterpret_cast<const CT*>(&vb);
+    // remainder (< 4 slots per lane): predicated loads, all issued before the adds
+    uint4 va[4], vb[4];
 #pragma unroll
-      for (int e = 0; e < VE; ++e) {
-        a[e] += static_cast<double>(pa[e]);
-        b[e] += static_cast<double>(pb[e]);
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = i + SL * u < n;
+      va[u] = ok ? __ldcg(reinterpret_cast<const uint4*>(sc + off(i + SL * u))) : make_uint4(0, 0, 0, 0);
+      vb[u] = ok ? __ldcg(reinterpret_cast<const uint4*>(sh + off(i + SL * u))) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i + SL * u < n) {
+        const CT* pa = reinterpret_cast<const CT*>(&va[u]);
+        const CT* pb = reinterpret_cast<const CT*>(&vb[u]);
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+          a[e] += static_cast<double>(pa[e]);
+          b[e] += static_cast<double>(pb[e]);
+        }
       }
     }
   }
-  // half-warp (slot lanes 2w, 2w+1) combine, fixed order: lower half + upper half
+  // slot lanes of a warp (lane / CV) combined by a fixed tree: lanes < CV end with the sum
 #pragma unroll
-  for (int e = 0; e < VE; ++e) {
-    const double ua = __shfl_down_sync(0xffffffffu, a[e], 16);
-    const double ub = __shfl_down_sync(0xffffffffu, b[e], 16);
-    if ((t & 31) < 16) {
-      part[0][warp][hl * VE + e] = a[e] + ua;
-      part[1][warp][hl * VE + e] = b[e] + ub;
+  for (int o = 16; o >= CV; o >>= 1) {
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      a[e] += __shfl_down_sync(0xffffffffu, a[e], o);
+      b[e] += __shfl_down_sync(0xffffffffu, b[e], o);
+    }
+  }
+  if ((t & 31) < CV) {
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      part[0][warp][hl * VE + e] = a[e];
+      part[1][warp][hl * VE + e] = b[e];
     }
   }
   __syncthreads();
+  pdl_launch();
   if (t < (two ? 2 : 1) * COLS) {
     const int which = t / COLS, c = t % COLS;
     const int64_t oc = static_cast<int64_t>(blockIdx.x) * COLS + c;
     if (oc < D) {
       double s = 0.0;
 #pragma unroll 8
-      for (int q = 0; q < 32; ++q) s += part[which][q][c];
+      for (int q = 0; q < NW; ++q) s += part[which][q][c];
       (which == 0 ? dscale : dshift)[g * D + oc] = static_cast<CT>(s);
     }
+  }
+  if (ts != nullptr) {
+    __syncthreads();
+    if (t == 0) ts_end(ts);
   }
 }
 

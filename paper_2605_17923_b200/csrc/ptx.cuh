@@ -104,6 +104,14 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Split form for short kernels that sit right before a PDL-launched persistent kernel (the
+// backward stage-2 reduction before the next forward): launching the dependent grid only once
+// this kernel's loads are done keeps the dependent's CTAs (which would only spin in their
+// griddepcontrol.wait) from taking the SM slots this kernel still needs.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // Per-CTA start/end timestamps (%globaltimer, ns) for tail/imbalance studies; compiled only
 // into trace builds (-DAL_CTA_TRACE, tools/ab_variant.sh), read by al_debug_cta_trace.
@@ -118,6 +126,23 @@ __device__ __forceinline__ void cta_trace(int kernel, int which) {
 #else
 #define AL_TRACE(kernel, which) ((void)0)
 #endif
+
+// Per-launch device timestamps (al_debug_set_timestamps): ts[0] = earliest CTA start,
+// ts[1] = latest CTA end (%globaltimer, ns), each CTA contributing one atomic at its start and
+// one at its end -- the kernel's own execution span, with nothing inserted into the stream
+// (an event record between two kernels costs ~5 us here: it breaks the PDL overlap).
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ts_begin(unsigned long long* ts) {
+  if (ts != nullptr && threadIdx.x == 0) atomicMin(ts, globaltimer_ns());
+}
+// call from ONE thread of the CTA after all of the CTA's work (behind a CTA / named barrier)
+__device__ __forceinline__ void ts_end(unsigned long long* ts) {
+  if (ts != nullptr) atomicMax(ts + 1, globaltimer_ns());
+}
 
 // 32-bit shared-window address form: no generic->shared conversion per access.
 __device__ __forceinline__ uint4 ld_shared_v4_u32(uint32_t a) {
