@@ -13,6 +13,8 @@ deterministic for a given chunking.
 
 from __future__ import annotations
 
+import threading
+
 import torch
 
 from ..errors import NonFiniteInput
@@ -43,8 +45,48 @@ def _chunks(b: int, s: int, row_bytes: int):
             yield b0, min(b, b0 + per), 0, s
 
 
+class _PinnedPool:
+    """Page-locked host result buffers, reused across calls.
+
+    A fresh ``torch.empty(pin_memory=True)`` of a few hundred MB goes through cudaHostAlloc
+    whenever torch's caching host allocator has no free block of that size class, which stalls
+    the call for 40-120 ms (round-1 driver e2e: 22 ms typical steps, 60-140 ms outliers).  Here
+    a buffer is handed out again only once nothing outside the pool references its storage (the
+    caller dropped the previous results, views and numpy aliases included), so results stay
+    valid for as long as the caller keeps them; at most ``MAX_PER_SIZE`` buffers are kept per
+    size, beyond that a call falls back to a one-off allocation."""
+
+    MAX_PER_SIZE = 4
+
+    def __init__(self):
+        self._bufs: dict = {}
+        self._lock = threading.Lock()
+
+    @staticmethod
+    def _free(buf: torch.Tensor) -> bool:
+        # references: the pool's tensor + the temporary storage wrapper of this query
+        return torch._C._storage_Use_Count(buf.untyped_storage()._cdata) <= 2
+
+    def get(self, shape, dtype) -> torch.Tensor:
+        numel = 1
+        for d in shape:
+            numel *= int(d)
+        nbytes = max(numel * torch.empty((), dtype=dtype).element_size(), 1)
+        with self._lock:
+            lst = self._bufs.setdefault(nbytes, [])
+            buf = next((b for b in lst if self._free(b)), None)
+            if buf is None:
+                buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+                if len(lst) < self.MAX_PER_SIZE:
+                    lst.append(buf)
+        return buf.view(dtype)[:numel].view(shape)
+
+
+_pool = _PinnedPool()
+
+
 def _pinned_like(shape, dtype):
-    return torch.empty(shape, dtype=dtype, pin_memory=True)
+    return _pool.get(tuple(shape), dtype)
 
 
 def host_forward(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor, eps: float,

@@ -73,6 +73,26 @@ def _stream_ptr(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+class _NoGuard:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NO_GUARD = _NoGuard()
+
+
+def _on(device: torch.device):
+    """Make `device` current around a library call: the C ABI plans and launches on the CUDA
+    current device (cudaGetDevice), and the stream it gets belongs to `device`.  A no-op when
+    `device` is already current (the common case), so the guard costs one query per call."""
+    if torch.cuda.current_device() == device.index:
+        return _NO_GUARD
+    return torch.cuda.device(device)
+
+
 def _prep(t: torch.Tensor, dt: torch.dtype, device: torch.device) -> torch.Tensor:
     if t.device != device:
         raise ShapeMismatch(f"all tensors must be on {device}, got {t.device}")
@@ -122,10 +142,11 @@ def fused_forward(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor, eps
     own_flag = check_finite and flag is None
     if own_flag:
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    rc = nat.load().al_adaln_forward(
-        x.data_ptr(), scale.data_ptr(), shift.data_ptr(), y.data_ptr(), mean.data_ptr(),
-        rstd.data_ptr(), g.batch, g.seq, g.dim, g.mod_stride, dtype_code(x.dtype), float(eps),
-        flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
+    with _on(dev):
+        rc = nat.load().al_adaln_forward(
+            x.data_ptr(), scale.data_ptr(), shift.data_ptr(), y.data_ptr(), mean.data_ptr(),
+            rstd.data_ptr(), g.batch, g.seq, g.dim, g.mod_stride, dtype_code(x.dtype), float(eps),
+            flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
     nat.check(rc, "al_adaln_forward")
     if own_flag:
         _raise_if_flagged(flag, "x/scale/shift")
@@ -163,11 +184,12 @@ def fused_gate_residual_forward(x: torch.Tensor, f: torch.Tensor, gate: torch.Te
     own_flag = check_finite and flag is None
     if own_flag:
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    rc = nat.load().al_adaln_gate_residual_forward(
-        x.data_ptr(), f.data_ptr(), gate.data_ptr(), scale.data_ptr(), shift.data_ptr(),
-        x_out.data_ptr(), y.data_ptr(), mean.data_ptr(), rstd.data_ptr(), g.batch, g.seq, g.dim,
-        g.mod_stride, dtype_code(x.dtype), float(eps),
-        flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
+    with _on(dev):
+        rc = nat.load().al_adaln_gate_residual_forward(
+            x.data_ptr(), f.data_ptr(), gate.data_ptr(), scale.data_ptr(), shift.data_ptr(),
+            x_out.data_ptr(), y.data_ptr(), mean.data_ptr(), rstd.data_ptr(), g.batch, g.seq, g.dim,
+            g.mod_stride, dtype_code(x.dtype), float(eps),
+            flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
     nat.check(rc, "al_adaln_gate_residual_forward")
     if own_flag:
         _raise_if_flagged(flag, "x/f/gate/scale/shift")
@@ -177,8 +199,9 @@ def fused_gate_residual_forward(x: torch.Tensor, f: torch.Tensor, gate: torch.Te
 def backward_workspace_bytes(x: torch.Tensor, scale: torch.Tensor, n_tile: int = 0) -> int:
     """Bytes of scratch fused_backward needs for these shapes (al_adaln_backward_workspace_bytes)."""
     g = geometry(x, scale)
-    n = nat.load().al_adaln_backward_workspace_bytes(g.batch, g.seq, g.dim, g.mod_stride,
-                                                      dtype_code(x.dtype), n_tile)
+    with _on(x.device):
+        n = nat.load().al_adaln_backward_workspace_bytes(g.batch, g.seq, g.dim, g.mod_stride,
+                                                          dtype_code(x.dtype), n_tile)
     if n < 0:
         nat.check(nat.AL_ERR_SHAPE, "al_adaln_backward_workspace_bytes")
     return max(int(n), 16)
@@ -216,8 +239,9 @@ def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean:
     rstd = _prep(rstd, sdt, dev)
     lib = nat.load()
     code = dtype_code(x.dtype)
-    ws_bytes = lib.al_adaln_backward_workspace_bytes(g.batch, g.seq, g.dim, g.mod_stride, code,
-                                                     n_tile)
+    with _on(dev):
+        ws_bytes = lib.al_adaln_backward_workspace_bytes(g.batch, g.seq, g.dim, g.mod_stride,
+                                                         code, n_tile)
     if ws_bytes < 0:
         nat.check(nat.AL_ERR_SHAPE, "al_adaln_backward_workspace_bytes")
     if workspace is None:
@@ -234,12 +258,13 @@ def fused_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mean:
     own_flag = check_finite and flag is None
     if own_flag:
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    rc = lib.al_adaln_backward(
-        dy.data_ptr(), x.data_ptr(), scale.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
-        dx.data_ptr(), dscale.data_ptr(), dshift.data_ptr(), ws.data_ptr(), int(ws_bytes),
-        g.batch, g.seq, g.dim, g.mod_stride, code, d_tile, n_tile,
-        nat.AL_BWD_DETERMINISTIC if deterministic else 0,
-        flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
+    with _on(dev):
+        rc = lib.al_adaln_backward(
+            dy.data_ptr(), x.data_ptr(), scale.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+            dx.data_ptr(), dscale.data_ptr(), dshift.data_ptr(), ws.data_ptr(), int(ws_bytes),
+            g.batch, g.seq, g.dim, g.mod_stride, code, d_tile, n_tile,
+            nat.AL_BWD_DETERMINISTIC if deterministic else 0,
+            flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
     nat.check(rc, "al_adaln_backward")
     if own_flag:
         _raise_if_flagged(flag, "dy/x/scale")
@@ -273,10 +298,11 @@ def fused_qk_rmsnorm_forward(qkv: torch.Tensor, wq: torch.Tensor, wk: torch.Tens
     vc = torch.empty_like(qn) if copy_v else None
     rstd = torch.empty(*lead, 2, dtype=stat_dtype(qkv.dtype), device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
-    rc = nat.load().al_qk_rmsnorm_forward(
-        qkv.data_ptr(), 3 * d, wq.data_ptr(), wk.data_ptr(), qn.data_ptr(), kn.data_ptr(),
-        vc.data_ptr() if vc is not None else None, rstd.data_ptr(), n, d, dtype_code(qkv.dtype),
-        float(eps), flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
+    with _on(dev):
+        rc = nat.load().al_qk_rmsnorm_forward(
+            qkv.data_ptr(), 3 * d, wq.data_ptr(), wk.data_ptr(), qn.data_ptr(), kn.data_ptr(),
+            vc.data_ptr() if vc is not None else None, rstd.data_ptr(), n, d, dtype_code(qkv.dtype),
+            float(eps), flag.data_ptr() if flag is not None else None, _stream_ptr(dev))
     nat.check(rc, "al_qk_rmsnorm_forward")
     _raise_if_flagged(flag, "qkv")
     return qn, kn, vc, rstd
@@ -301,18 +327,20 @@ def fused_qk_rmsnorm_backward(qkv: torch.Tensor, wq: torch.Tensor, wk: torch.Ten
     n = qkv.numel() // (3 * d) if qkv.numel() else 0
     lib = nat.load()
     code = dtype_code(qkv.dtype)
-    ws_bytes = lib.al_qk_rmsnorm_backward_workspace_bytes(n, d, code)
+    with _on(dev):
+        ws_bytes = lib.al_qk_rmsnorm_backward_workspace_bytes(n, d, code)
     if ws_bytes < 0:
         nat.check(nat.AL_ERR_SHAPE, "al_qk_rmsnorm_backward_workspace_bytes")
     ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
     dqkv = torch.empty_like(qkv) if dv is not None else torch.zeros_like(qkv)
     dwq = torch.empty(d, dtype=sdt, device=dev)
     dwk = torch.empty(d, dtype=sdt, device=dev)
-    rc = lib.al_qk_rmsnorm_backward(
-        qkv.data_ptr(), 3 * d, wq.data_ptr(), wk.data_ptr(), rstd.data_ptr(), dqn.data_ptr(),
-        dkn.data_ptr(), dv.data_ptr() if dv is not None else None, dqkv.data_ptr(),
-        dwq.data_ptr(), dwk.data_ptr(), ws.data_ptr(), int(ws_bytes), n, d, code, None,
-        _stream_ptr(dev))
+    with _on(dev):
+        rc = lib.al_qk_rmsnorm_backward(
+            qkv.data_ptr(), 3 * d, wq.data_ptr(), wk.data_ptr(), rstd.data_ptr(), dqn.data_ptr(),
+            dkn.data_ptr(), dv.data_ptr() if dv is not None else None, dqkv.data_ptr(),
+            dwq.data_ptr(), dwk.data_ptr(), ws.data_ptr(), int(ws_bytes), n, d, code, None,
+            _stream_ptr(dev))
     nat.check(rc, "al_qk_rmsnorm_backward")
     return dqkv, dwq, dwk
 
@@ -332,16 +360,19 @@ def fused_gate_residual_backward(dxn: torch.Tensor, gxo: torch.Tensor | None, f:
         gxo = _prep(gxo, dt, dev)
     lib = nat.load()
     code = dtype_code(dt)
-    ws_bytes = lib.al_gate_residual_backward_workspace_bytes(g.batch, g.seq, g.dim, g.mod_stride, code)
+    with _on(dev):
+        ws_bytes = lib.al_gate_residual_backward_workspace_bytes(g.batch, g.seq, g.dim,
+                                                                 g.mod_stride, code)
     if ws_bytes < 0:
         nat.check(nat.AL_ERR_SHAPE, "al_gate_residual_backward_workspace_bytes")
     ws = torch.empty(max(int(ws_bytes), 16), dtype=torch.uint8, device=dev)
     dx = torch.empty_like(dxn)
     df = torch.empty_like(dxn)
     dgate = torch.empty(g.grad_shape, dtype=stat_dtype(dt), device=dev)
-    rc = lib.al_gate_residual_backward(
-        dxn.data_ptr(), gxo.data_ptr() if gxo is not None else None, f.data_ptr(),
-        gate.data_ptr(), dx.data_ptr(), df.data_ptr(), dgate.data_ptr(), ws.data_ptr(),
-        int(ws_bytes), g.batch, g.seq, g.dim, g.mod_stride, code, _stream_ptr(dev))
+    with _on(dev):
+        rc = lib.al_gate_residual_backward(
+            dxn.data_ptr(), gxo.data_ptr() if gxo is not None else None, f.data_ptr(),
+            gate.data_ptr(), dx.data_ptr(), df.data_ptr(), dgate.data_ptr(), ws.data_ptr(),
+            int(ws_bytes), g.batch, g.seq, g.dim, g.mod_stride, code, _stream_ptr(dev))
     nat.check(rc, "al_gate_residual_backward")
     return dx, df, dgate

@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <mutex>
+#include <unordered_map>
+#include <unordered_set>
 
 #include "../../include/adaln_b200.h"
 #include "adaln_kernels.cuh"
@@ -383,26 +385,21 @@ const void* reduce_kernel(int dtype, bool vec) {
   return vec ? (const void*)al::adaln_bwd_reduce_vec<float> : (const void*)al::adaln_bwd_reduce<float>;
 }
 
-// Per-(kernel image, device) one-time attribute setup.
+// Per-(kernel image, device) one-time attribute setup: a hash set per device (al_device_init
+// registers every kernel of the tables, ~600 per device).
 struct AttrCache {
   std::mutex mu;
-  const void* fn[512];
-  int dev[512];
-  int n = 0;
+  std::unordered_set<const void*> done[64];
 };
 AttrCache g_attr;
 
 int ensure_attr(const void* fn, int dev) {
+  if (dev < 0 || dev >= 64) return fail(AL_ERR_CUDA, "device ordinal %d out of range", dev);
   std::lock_guard<std::mutex> lk(g_attr.mu);
-  for (int i = 0; i < g_attr.n; ++i)
-    if (g_attr.fn[i] == fn && g_attr.dev[i] == dev) return AL_OK;
+  if (g_attr.done[dev].count(fn)) return AL_OK;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-  if (g_attr.n < 512) {
-    g_attr.fn[g_attr.n] = fn;
-    g_attr.dev[g_attr.n] = dev;
-    ++g_attr.n;
-  }
+  g_attr.done[dev].insert(fn);
   return AL_OK;
 }
 
@@ -714,13 +711,25 @@ unsigned long long* next_ts() {
 }
 
 // ---------------------------------------------------------------- dynamic row tail
-// Ticket-counter slot for one dynamically scheduled launch (al::g_sched, zero-initialised
-// module memory; the launch's last CTA re-arms it).  Slots go round-robin, so launches in
-// flight on different streams use different counters as long as fewer than kSchedSlots are
-// outstanding at once.
-std::atomic<unsigned int> g_sched_seq{0};
+// Ticket-counter slot for one dynamically scheduled launch (al::g_sched, zero-initialised module
+// memory, one array per device; the launch's last CTA re-arms its slot).
+//  * Eager launches: one slot per (device, stream).  Launches on one stream run in stream order
+//    (each kernel's griddepcontrol.wait precedes its first ticket), so the previous launch has
+//    re-armed the slot before the next one draws from it; launches on different streams never
+//    share a counter.
+//  * Launches being captured into a CUDA graph: a slot of their own that is never handed out
+//    again (the slot is baked into the graph node; replays of one graph exec are serialised by
+//    CUDA, and eager launches cannot collide with it).
+// When the slots run out, the launch runs without the dynamic tail (static partition: same
+// results, fewer GB/s) -- never a shared counter.
+struct SchedSlots {
+  std::mutex mu;
+  unsigned int next[64] = {};
+  std::unordered_map<uintptr_t, unsigned int> by_stream[64];
+};
+SchedSlots g_slots;
 
-unsigned int* sched_slot(int dev) {
+unsigned int* sched_slot(int dev, cudaStream_t st) {
   static std::atomic<unsigned int*> base[64] = {};
   if (dev < 0 || dev >= 64) return nullptr;
   unsigned int* b = base[dev].load(std::memory_order_acquire);
@@ -733,7 +742,26 @@ unsigned int* sched_slot(int dev) {
     b = static_cast<unsigned int*>(ptr);
     base[dev].store(b, std::memory_order_release);  // same value from any racing thread
   }
-  const unsigned int slot = g_sched_seq.fetch_add(1u) % al::kSchedSlots;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_slots.mu);
+  unsigned int slot;
+  if (cap == cudaStreamCaptureStatusNone) {
+    auto it = g_slots.by_stream[dev].find(reinterpret_cast<uintptr_t>(st));
+    if (it != g_slots.by_stream[dev].end()) {
+      slot = it->second;
+    } else {
+      if (g_slots.next[dev] >= static_cast<unsigned int>(al::kSchedSlots)) return nullptr;
+      slot = g_slots.next[dev]++;
+      g_slots.by_stream[dev].emplace(reinterpret_cast<uintptr_t>(st), slot);
+    }
+  } else {
+    if (g_slots.next[dev] >= static_cast<unsigned int>(al::kSchedSlots)) return nullptr;
+    slot = g_slots.next[dev]++;
+  }
   return b + 2 * slot;
 }
 
@@ -762,7 +790,7 @@ double bwd_dyn_frac() {
   return f;
 }
 
-void enable_dynamic_tail(const Plan& pl, al::FwdParams& p) {
+void enable_dynamic_tail(const Plan& pl, al::FwdParams& p, cudaStream_t st) {
   const double f = fwd_dyn_frac();
   if (!(f > 0.0) || pl.path != 2 || pl.R != 2) return;
   const int64_t warps = static_cast<int64_t>(pl.grid) * (pl.threads / 32);
@@ -774,7 +802,7 @@ void enable_dynamic_tail(const Plan& pl, al::FwdParams& p) {
   if (n_dyn < 2 * warps) return;
   int dev;
   if (cudaGetDevice(&dev) != cudaSuccess) return;
-  unsigned int* slot = sched_slot(dev);
+  unsigned int* slot = sched_slot(dev, st);
   if (slot == nullptr) return;
   p.sched = slot;
   p.N_static = p.N - n_dyn;
@@ -1065,7 +1093,7 @@ int al_adaln_forward(const void* x, const void* scale, const void* shift, void* 
   al::FwdParams p = fwd_params(x, scale, shift, y, mean, rstd, seq, N, dim, mod_stride, dtype,
                                eps, nonfinite, pl);
   p.ts = next_ts();
-  enable_dynamic_tail(pl, p);
+  enable_dynamic_tail(pl, p, static_cast<cudaStream_t>(stream));
   return launch(pl, p, stream, "forward launch");
 }
 
@@ -1116,7 +1144,7 @@ int al_adaln_gate_residual_forward(const void* x, const void* f, const void* gat
       p.f = f;
       p.gate = gate;
       p.x_out = x_out;
-      enable_dynamic_tail(pr, p);
+      enable_dynamic_tail(pr, p, static_cast<cudaStream_t>(stream));
       return launch(pr, p, stream, "gate-residual forward launch");
     }
   }
@@ -1209,6 +1237,11 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
     // they gain (cfg3 S = 1 560: 34.2 vs 29.0 us fwd+bwd; break-even near S = 10 000 at
     // D = 5 120): >= 64 tail rows per CTA
     if (n_dyn < 64 * static_cast<int64_t>(pl.grid)) n_dyn = 0;
+    // stage 2 sums the static slots of every CTA between the owners of a group's first and last
+    // static rows; with 0 < N_static < G some of those CTAs would own no rows and never write
+    // their slot, so a static head is either empty or at least one row per CTA
+    const int64_t n_static = N - n_dyn;
+    if (n_static > 0 && n_static < pl.grid) n_dyn = 0;
   }
   const int64_t nslots = nslots_static + (n_dyn ? pl.grid : 0);
   const int64_t need = 2 * nslots * dim * cs;
@@ -1247,7 +1280,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
     const void* dfn = tma_dyn_kernel(dtype, pl.V, pl.R, full);
     unsigned int* slot = nullptr;
     if (dfn && cudaGetDevice(&dev) == cudaSuccess && ensure_attr(dfn, dev) == AL_OK)
-      slot = sched_slot(dev);
+      slot = sched_slot(dev, st);
     if (slot) {
       pl.fn = dfn;
       p.sched = slot;

@@ -63,9 +63,10 @@ struct FwdParams {
   unsigned long long* ts;  // nullable: per-launch device timestamps (ptx.cuh ts_begin/ts_end)
 };
 
-// Ticket-counter slots for dynamically scheduled launches; the host hands launches slots
-// round-robin, and the last CTA of each launch resets its slot to zero.
-constexpr int kSchedSlots = 1024;
+// Ticket-counter slots for dynamically scheduled launches: one per (device, stream) for eager
+// launches and one per captured launch (adaln_capi.cu sched_slot); the last CTA of each launch
+// resets its slot to zero.
+constexpr int kSchedSlots = 16384;
 __device__ unsigned int g_sched[kSchedSlots][2];
 
 struct BwdParams {

@@ -91,7 +91,9 @@ class WanStyleBlock(nn.Module):
         shift1, scale1, gate1, shift2, scale2, gate2 = e.unbind(1)
         y = self.norm_fn(x, scale1.contiguous(), shift1.contiguous(), self.cfg.eps)
         qkv = self.qkv(y)
-        if self.qk_norm_fn is not None:
+        # the fused Q/K norm holds a whole row in one warp's registers: rows of <= 4 KB (bf16
+        # D <= 2048, the Wan-1.3B width); wider blocks (Wan-14B D = 5120) take nn.RMSNorm
+        if self.qk_norm_fn is not None and d * qkv.element_size() <= 4096:
             q, k, v = self.qk_norm_fn(qkv, self.q_norm.weight, self.k_norm.weight, self.cfg.eps)
         else:
             q, k, v = qkv.split(d, dim=-1)
