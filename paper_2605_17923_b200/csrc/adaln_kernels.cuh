@@ -568,12 +568,10 @@ __global__ void __launch_bounds__(256) adaln_fwd_rows2(const FwdParams p) {
 
 // =====================================================================================
 // Forward, row-in-registers path for 16-bit rows (bf16 / fp16): the row stays packed in
-// registers and is consumed by mixed-precision subtracts (FHADD.{BF16,F16}: 16-bit operand,
-// fp32 result), so there is no separate expansion step.  Statistics in one pass over the
-// shifted values d = x - K (K = the row's first element): mean = K + sum(d)/D and
-// M2 = sum(d^2) - sum(d)^2/D -- the shift keeps the cancellation at the level of
-// (K - mean)^2 / var, far below the 16-bit inputs' own rounding.  Second pass writes
-// y = (x - mean) * rstd * (1 + scale) + shift.  About 5 instructions per element instead of 8.
+// registers and is consumed by mixed-precision adds (FHADD.{BF16,F16}: 16-bit operand, fp32
+// result), so there is no separate expansion step.  Exact two-pass statistics from the
+// registers (mean, then the centred sum of squares), then y = (x - mean) * rstd * (1 + scale)
+// + shift.  About 5.5 instructions per element instead of 8 for the unpacking kernel.
 // =====================================================================================
 template <typename T, int VPL, bool RESID = false>
 __global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
@@ -640,29 +638,40 @@ __global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
         v[i] = pack2<T>(xa);
       }
     }
-    P k0[NP];
-    unpack2<T>(v[0], k0);
-    const float K = __shfl_sync(0xffffffffu, k0[0].x, 0);
-    // pass 1: sum(d), sum(d^2) over valid vectors
-    P s[2] = {splat2(0.0f), splat2(0.0f)}, q[2] = {splat2(0.0f), splat2(0.0f)};
+    // Exact two-pass statistics from the register-resident row (the reference's order of
+    // operations, _kernels_numba.py:22-30): pass 1 the mean, pass 2 the centred sum of squares
+    // -- no E[x^2] - E[x]^2 cancellation whatever the row's offset or outliers.  Both passes
+    // read the packed 16-bit row through mixed-precision adds (FHADD: 16-bit operand, fp32
+    // result), so neither needs an unpack step.
+    float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       if (lane + 32 * i < p.nvec) {
         const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const P dd = sub16x2_f32<T>(w[e], -K);
-          s[e & 1] = add2(s[e & 1], dd);
+          const float2 a = acc16x2_f32<T>(w[e], make_float2(s4[(2 * e) & 3], s4[(2 * e + 1) & 3]));
+          s4[(2 * e) & 3] = a.x;
+          s4[(2 * e + 1) & 3] = a.y;
+        }
+      }
+    }
+    const float mean = warp_sum((s4[0] + s4[1]) + (s4[2] + s4[3])) * invD;
+    P q[2] = {splat2(0.0f), splat2(0.0f)};
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      if (lane + 32 * i < p.nvec) {
+        const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const P dd = sub16x2_f32<T>(w[e], -mean);
           q[e & 1] = fma2(dd, dd, q[e & 1]);
         }
       }
     }
-    const P ts = add2(s[0], s[1]), tq = add2(q[0], q[1]);
-    const float sd = warp_sum(ts.x + ts.y);
+    const P tq = add2(q[0], q[1]);
     const float sq = warp_sum(tq.x + tq.y);
-    const float md = sd * invD;
-    const float m2 = fmaxf(sq - sd * md, 0.0f);
-    const float mean = K + md;
+    const float m2 = sq;
     const float rs = 1.0f / sqrtf(m2 * invD + eps);
     const P rs2 = splat2(rs);
     // pass 2: y = (x - mean) * rstd * (1 + scale) + shift
@@ -984,12 +993,9 @@ __global__ void __launch_bounds__(512) adaln_fwd_wide(const FwdParams p) {
 // sums are reduce-scattered within the warp and combined across warps through a named barrier,
 // the slot is released, and y = (x - mean) * rstd * (1 + scale) + shift is written from the
 // registers.  Packed fp32 pair math; (1 + scale, shift) of the owned columns live in registers.
-// Statistics of d = x - K (K = the row's first element):
-//   16-bit rows: one pass of sum d and sum d^2 (d exact in fp32; the cancellation error
-//     ~2^-24 sqrt(D) (1 + (K - mean)^2 / var) is far below the 2^-9 output rounding);
-//   32/64-bit rows: exact two passes from the registers (sum d, barrier, sum (d - mean_d)^2,
-//     barrier) -- a single pass can exceed 1e-5 relative on rows whose first element is a
-//     far outlier.
+// Statistics of d = x - K (K = the row's first element), exact two passes from the registers
+// (sum d, barrier, sum (d - mean_d)^2, barrier) for every dtype -- a single pass of sum d and
+// sum d^2 can lose the variance of rows whose first element is a far outlier.
 // =====================================================================================
 template <typename T, int V, int R>
 __global__ void __launch_bounds__(384) adaln_fwd_ring(const FwdParams p) {
@@ -997,7 +1003,7 @@ __global__ void __launch_bounds__(384) adaln_fwd_ring(const FwdParams p) {
   using CT = typename Traits<T>::CT;
   using P = typename PairOf<CT>::type;
   constexpr int NP = Traits<T>::EPV / 2;
-  constexpr bool TWO = sizeof(T) >= 4;
+  constexpr bool TWO = true;  // exact two-pass statistics (the one-pass branch is kept for A/B)
   constexpr int NV = TWO ? R : 2 * R;  // row sums reduced per barrier
   extern __shared__ __align__(128) uint8_t smem[];
 

@@ -273,6 +273,24 @@ __device__ __forceinline__ float2 sub16x2_f32(uint32_t w, float nk) {
   return make_float2(a, b);
 }
 
+// acc + x16 for both halves of a packed pair (FHADD with per-half fp32 accumulators): the
+// 16-bit row summed without unpacking it
+template <typename T>
+__device__ __forceinline__ float2 acc16x2_f32(uint32_t w, float2 acc) {
+  static_assert(sizeof(T) == 2, "16-bit types only");
+  unsigned short lo, hi;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(w));
+  float a, b;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    asm("add.rn.f32.bf16 %0, %1, %2;" : "=f"(a) : "h"(lo), "f"(acc.x));
+    asm("add.rn.f32.bf16 %0, %1, %2;" : "=f"(b) : "h"(hi), "f"(acc.y));
+  } else {
+    asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(a) : "h"(lo), "f"(acc.x));
+    asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(b) : "h"(hi), "f"(acc.y));
+  }
+  return make_float2(a, b);
+}
+
 template <typename CT>
 __device__ __forceinline__ bool finite_ct(CT v) {
   return isfinite(v);
