@@ -12,18 +12,97 @@ import csv
 import json
 from pathlib import Path
 
+from dataclasses import dataclass
+
 from .costfit import CostModel, Trial
+from .manifest import RunManifest
 from .scheduler import Binding, BucketPlan, PlanEntry
-from .shapes import Bucket, MediaShape
+from .shapes import Bucket, LatentGeometry, MediaShape, build_catalog
 
 __all__ = ["save_trace", "load_trace", "save_plan", "load_plan", "save_model", "load_model",
-           "save_metrics_csv", "METRICS_COLUMNS", "trials_from_steps"]
+           "save_metrics_csv", "METRICS_COLUMNS", "trials_from_steps", "load_catalog",
+           "save_catalog", "ClusterCost", "ClusterConfig", "load_cluster_config", "save_summary",
+           "write_manifest_sidecar"]
 
 METRICS_COLUMNS = ["step", "policy", "t_sync", "cv_step", "compute_cv", "tokens_per_sec", "theta"]
 
 
 def _write_json(path, doc) -> None:
     Path(path).write_text(json.dumps(doc, sort_keys=True, indent=2) + "\n")
+
+
+def _manifest_doc(manifest) -> dict:
+    if manifest is None:
+        return {}
+    return manifest.to_dict() if isinstance(manifest, RunManifest) else dict(manifest)
+
+
+def write_manifest_sidecar(path, manifest) -> None:
+    """Manifest of a line/row-oriented artifact (JSONL, CSV) in ``<path>.manifest.json``."""
+    _write_json(str(path) + ".manifest.json", _manifest_doc(manifest))
+
+
+# ------------------------------------------------------------------ catalogs (io.py:32-80)
+_GEOM_DEFAULTS = {"temporal_factor": 8, "width_factor": 16, "height_factor": 16, "text_tokens": 0}
+
+
+def load_catalog(path):
+    """(buckets, weights, geometry) from a catalog JSON: either a list of
+    {frames, height, width, count} or {"shapes": [...], "geometry": {...}} (missing geometry
+    keys take the reference defaults); weights are the normalised sample counts."""
+    doc = json.loads(Path(path).read_text())
+    shapes, geom_doc = (doc, {}) if isinstance(doc, list) else (doc["shapes"], doc.get("geometry", {}))
+    g = {k: geom_doc.get(k, v) for k, v in _GEOM_DEFAULTS.items()}
+    geom = LatentGeometry(temporal_factor=g["temporal_factor"], width_factor=g["width_factor"],
+                          height_factor=g["height_factor"], text_tokens=g["text_tokens"])
+    catalog = build_catalog([(MediaShape(r["frames"], r["height"], r["width"]), r["count"])
+                             for r in shapes], geom)
+    n = sum(b.sample_count for b in catalog)
+    return catalog, [b.sample_count / n for b in catalog], geom
+
+
+def save_catalog(path, catalog, geom: LatentGeometry) -> None:
+    _write_json(path, {
+        "shapes": [{"frames": b.shape.frames, "height": b.shape.height, "width": b.shape.width,
+                    "count": b.sample_count} for b in catalog],
+        "geometry": {k: getattr(geom, k) for k in _GEOM_DEFAULTS}})
+
+
+# ------------------------------------------------------------ cluster config (io.py:83-96)
+@dataclass(frozen=True)
+class ClusterCost:
+    a: float = 2.0
+    b: float = 1e-9
+    p: float = 2.0
+
+
+@dataclass(frozen=True)
+class ClusterConfig:
+    """The reference simulator's cluster description (cluster_sim.py:53-63); on B200 the DP
+    step takes its world size from torch.distributed and measures the per-rank cost, so only
+    num_workers / seed / steps steer a run, the cost block is carried for the reference tools."""
+
+    num_workers: int = 16
+    cost: ClusterCost = ClusterCost()
+    noise_sigma: float = 0.03
+    seed: int = 42
+    steps: int = 500
+
+
+def load_cluster_config(path, seed_override: int | None = None) -> ClusterConfig:
+    doc = json.loads(Path(path).read_text())
+    c = doc.get("cost", {})
+    d = ClusterConfig()
+    return ClusterConfig(
+        num_workers=doc.get("num_workers", d.num_workers),
+        cost=ClusterCost(c.get("a", d.cost.a), c.get("b", d.cost.b), c.get("p", d.cost.p)),
+        noise_sigma=doc.get("noise_sigma", d.noise_sigma),
+        seed=doc.get("seed", d.seed) if seed_override is None else seed_override,
+        steps=doc.get("steps", d.steps))
+
+
+def save_summary(path, summary: dict, manifest=None) -> None:
+    _write_json(path, {**summary, "manifest": _manifest_doc(manifest)})
 
 
 def save_trace(path, trials, workers=None) -> None:
@@ -46,13 +125,13 @@ def load_trace(path) -> list:
     return out
 
 
-def save_plan(path, plan: BucketPlan, manifest: dict | None = None) -> None:
+def save_plan(path, plan: BucketPlan, manifest=None) -> None:
     entries = [{"frames": e.bucket.shape.frames, "height": e.bucket.shape.height,
                 "width": e.bucket.shape.width, "seq_len": e.bucket.seq_len,
                 "sample_count": e.bucket.sample_count, "batch_size": e.batch_size,
                 "binding": None if e.binding is None else e.binding.value}
                for e in plan.entries]
-    _write_json(path, {"entries": entries, "manifest": manifest or {}})
+    _write_json(path, {"entries": entries, "manifest": _manifest_doc(manifest)})
 
 
 def load_plan(path) -> BucketPlan:
@@ -64,9 +143,9 @@ def load_plan(path) -> BucketPlan:
         for e in doc["entries"]))
 
 
-def save_model(path, model: CostModel, manifest: dict | None = None) -> None:
+def save_model(path, model: CostModel, manifest=None) -> None:
     _write_json(path, {"a": model.a, "b": model.b, "p": model.p, "r2": model.r2,
-                       "manifest": manifest or {}})
+                       "manifest": _manifest_doc(manifest)})
 
 
 def load_model(path) -> CostModel:

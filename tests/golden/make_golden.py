@@ -258,8 +258,80 @@ def make_io():
     rio.save_metrics_csv(d / "metrics.csv", {"equal_token": res.series_a, "dual": res.series_b})
 
 
+def make_io_r2():
+    """Round 2: catalog / cluster-config / summary / manifest files and config digests written
+    or computed by the reference's io.py and manifest.py (tests/golden/io/)."""
+    from adaptiveload import io as rio
+    from adaptiveload.costfit import analyze_bottleneck
+    from adaptiveload.manifest import RunManifest, config_digest
+
+    d = OUT / "io"
+    d.mkdir(exist_ok=True)
+    cat, _ = default_catalog()
+    rio.save_catalog(d / "catalog_default.json", cat, LatentGeometry())
+    geom4 = LatentGeometry(temporal_factor=4, width_factor=16, height_factor=16, text_tokens=0)
+    wan = build_catalog([(MediaShape(1, 480, 832), 40), (MediaShape(81, 480, 832), 4),
+                         (MediaShape(81, 720, 1280), 2)], geom4)
+    rio.save_catalog(d / "catalog_wan_l4.json", wan, geom4)
+    (d / "catalog_list.json").write_text(json.dumps(
+        [{"frames": 17, "height": 640, "width": 640, "count": 5},
+         {"frames": 1, "height": 640, "width": 640, "count": 15}]))
+    loaded = {}
+    for name in ("catalog_default.json", "catalog_wan_l4.json", "catalog_list.json"):
+        c, w, g = rio.load_catalog(d / name)
+        loaded[name] = {"seq": [b.seq_len for b in c], "count": [b.sample_count for b in c],
+                        "weights": w, "geometry": [g.temporal_factor, g.width_factor,
+                                                   g.height_factor, g.text_tokens]}
+    (d / "cluster_partial.json").write_text(json.dumps({"num_workers": 8, "cost": {"p": 1.5}}))
+    (d / "cluster_full.json").write_text(json.dumps(
+        {"num_workers": 4, "cost": {"a": 1.0, "b": 2e-9, "p": 2.2}, "noise_sigma": 0.0,
+         "seed": 7, "steps": 40}))
+    clusters = {}
+    for name, seed in (("cluster_partial.json", None), ("cluster_full.json", None),
+                       ("cluster_full.json", 99)):
+        c = rio.load_cluster_config(d / name, seed_override=seed)
+        clusters[f"{name}:{seed}"] = [c.num_workers, c.cost.a, c.cost.b, c.cost.p, c.noise_sigma,
+                                      c.seed, c.steps]
+    man = RunManifest(command="simulate", inputs=["catalog.json", "cluster.json"],
+                      outputs=["summary.json"], seed=42,
+                      config_digest=config_digest({"policy": "dual", "m_comp": 3e9, "p": 2.0}))
+    rio.save_summary(d / "summary.json", {"cv_step": 0.25, "tokens_per_sec": 1234.5,
+                                          "policies": ["equal_token", "dual"]}, man)
+    rio.write_manifest_sidecar(d / "trace.jsonl", man)
+    payloads = [{}, {"b": 1, "a": 2}, {"m_comp": 3e9, "p": 2.0, "policy": "dual"},
+                {"nested": {"z": [1, 2.5, None], "a": True}, "s": "x"}, [3, {"k": "v"}]]
+    digests = [[pl, config_digest(pl)] for pl in payloads]
+    # bottleneck analysis (costfit.py:209-232) on simulator-style wait records
+    from types import SimpleNamespace
+
+    from adaptiveload.costfit import CostModel
+
+    rng = np.random.default_rng(3)
+    waits = []
+    for _ in range(20):
+        t = rng.exponential(0.2, 8) + 1.0
+        waits.append([float(v) for v in (t.max() - t)])  # the straggler waits exactly 0
+    recs = [SimpleNamespace(per_worker=[SimpleNamespace(wait_sync=v) for v in row]) for row in waits]
+    bn = analyze_bottleneck(recs)
+    bn2 = analyze_bottleneck(recs, CostModel(a=2.0, b=1e-9, p=2.0, r2=1.0), 62.0)
+
+    def as_json(r):
+        return {"mean_wait": [float(v) for v in r.mean_wait],
+                "straggler_fraction": [float(v) for v in r.straggler_fraction],
+                "suggested_m_comp": r.suggested_m_comp}
+
+    bottleneck = {"waits": waits, "result": as_json(bn), "result_model": as_json(bn2)}
+    (d / "io_r2.json").write_text(json.dumps({"loaded_catalogs": loaded, "clusters": clusters,
+                                              "digests": digests, "bottleneck": bottleneck},
+                                             indent=1, sort_keys=True))
+
+
 if __name__ == "__main__":
-    make_adaln()
-    make_sampler()
-    make_io()
+    if sys.argv[1:] == ["io_r2"]:
+        make_io_r2()
+    else:
+        make_adaln()
+        make_sampler()
+        make_io()
+        make_io_r2()
     print("wrote", sorted(p.name for p in OUT.iterdir()))
