@@ -415,25 +415,28 @@ def run_ours(args, world, rank, local):
     d2h = (x.numel() * es + 2 * S * 4) + (x.numel() * es + 2 * D * 4)
     e2e_gbs = world * nb["total"] / e2e_s / 1e9
 
-    # measured 'N-GPU imbalance %' of the metric: the DP step A/B (equal-token vs the
-    # B200-calibrated dual constraint) on this process group, N > 1 only
+    # measured 'N-GPU imbalance %' of the metric: the DP step on this process group under
+    # each bucket plan (equal token, the reference's dual constraint, the reference fitter's
+    # power-law dual on B200 trials, the two-term time-balanced plan), N > 1 only
     dp = None
     if world > 1 and not args.no_dp:
-        del x, dy, xh, dyh, out, gr
+        del x, dy, xh, dyh, out, gr, y, dx, ws
         torch.cuda.empty_cache()
         try:
             from paper_2605_17923_b200 import dp_step
 
-            r = dp_step.run_ab(world, rank, local, steps=args.dp_steps, warmup=2, detail=False)
-            pol = r["policies"]
+            arms = tuple(a for a in args.dp_arms.split(",") if a)
+            r = dp_step.run_arms(world, rank, local, steps=args.dp_steps, warmup=2, arms=arms,
+                                 detail=False)
             dp = {"workload": r["config"]["workload"], "steps_per_policy": args.dp_steps,
-                  "plan_equal_token": r["config"]["plan_equal_token"],
-                  "plan_dual": r["config"]["plan_dual"], **r["imbalance"],
-                  "tokens_per_sec_equal_token": pol["equal_token"]["tokens_per_sec"],
-                  "tokens_per_sec_dual": pol["dual"]["tokens_per_sec"],
-                  "throughput_gain_vs_equal_token": r["throughput_gain_vs_equal_token"],
-                  "measured_ms_by_bucket_dual": pol["dual"]["measured_ms_by_bucket"],
-                  "predicted_ms_dual": (r["calibration"] or {}).get("predicted_ms")}
+                  "plans": r["config"]["plans"], "arms": r["config"]["arms"],
+                  "imbalance": r["imbalance"],
+                  "bottleneck": {a: r["policies"][a]["bottleneck"] for a in arms},
+                  "measured_ms_by_bucket": {a: r["policies"][a]["measured_ms_by_bucket"]
+                                            for a in arms},
+                  "calibration": (None if not r["calibration"] else
+                                  {k: r["calibration"][k] for k in ("power_fit", "quadratic_fit",
+                                                                    "predicted_ms")})}
         except Exception as exc:  # noqa: BLE001 - the kernel line must still be printed
             dp = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if rank != 0:
@@ -533,7 +536,13 @@ def main():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-dp", action="store_true", help="skip the N>1 DP-step imbalance A/B")
     ap.add_argument("--dp-steps", type=int, default=16)
+    ap.add_argument("--dp-arms", default="equal_token,dual_reference,dual_power_fit,dual_quadratic")
     args, rest = ap.parse_known_args()
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl == "ours":
+        # NCCL communicator init lines (nRanks, NVLS / channels) for the driver's rank count;
+        # NCCL reads these once, so they are set before anything imports torch
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup(args)
     try:

@@ -339,8 +339,11 @@ def run_policy_steps(runner: DPStepRunner, sampler: BucketSampler, steps: int,
 
 
 def summarize(stats: list, world: int) -> dict:
+    from .costfit import analyze_bottleneck
+
     tok = sum(s.tokens for s in stats)
     t = sum(s.t_step_ms for s in stats) / 1e3
+    bn = analyze_bottleneck(stats) if stats else None  # measured wait_sync per rank
     per_bucket = {}
     for st in stats:
         for sh, ti in zip(st.shards, st.t_compute_ms):
@@ -357,30 +360,46 @@ def summarize(stats: list, world: int) -> dict:
         "mean_cv_step_measured": float(np.mean([s.cv_step for s in stats])) if world > 1 else 0.0,
         "mean_compute_cv": float(np.mean([s.compute_cv for s in stats])) if world > 1 else 0.0,
         "mean_wait_sync_ms": float(np.mean([np.mean(s.wait_sync_ms) for s in stats])),
+        # reference costfit.analyze_bottleneck on the measured waits: mean wait per rank (ms)
+        # and the share of steps each rank was the straggler
+        "bottleneck": None if bn is None else {
+            "mean_wait_ms": [round(1e3 * v, 3) for v in bn.mean_wait],
+            "straggler_fraction": [round(v, 4) for v in bn.straggler_fraction]},
     }
 
 
 # ------------------------------------------------------------------------------ bench entry
-def run_ab(world: int, rank: int, local: int, steps: int, warmup: int, seed: int = 42,
-           token_budget: int = 480_000, m_comp: float = 0.0, plan_kind: str = "calibrated",
-           cost_model: str = "quadratic", detail: bool = True) -> dict:
-    """Equal-token vs dual-constraint A/B of the DP step on this process group.  Returns the
-    result dict on every rank (rank 0's calibration is broadcast so plans agree)."""
+ARMS = ("equal_token", "dual_reference", "dual_power_fit", "dual_quadratic")
+ARM_DOC = {
+    "equal_token": "TokenBudget(M_mem): B = floor(M_mem / S) (scheduler.py:95-98)",
+    "dual_reference": "the reference's DualConstraint(M_mem, 3e9 * (M_mem / 480k)^2, p = 2) "
+                      "(cluster_sim.py:332-336): plan [300, 100, 32, 5, 1, 1] at 480k",
+    "dual_power_fit": "the reference fitter on B200 trials: T = a + b B S^p grid-searched "
+                      "(costfit.py:116-140), M_comp from the fit (calibrated_dual_constraint)",
+    "dual_quadratic": "B200 two-term fit T = a + c1 B S + c2 B S^2, every bucket capped at the "
+                      "longest bucket's B = 1 time (costfit.time_balanced_plan)",
+}
+
+
+def run_arms(world: int, rank: int, local: int, steps: int, warmup: int, seed: int = 42,
+             token_budget: int = 480_000, m_comp: float = 0.0, arms=ARMS,
+             detail: bool = True, keep_stats: bool = False) -> dict:
+    """The DP step under each bucket plan in `arms`, same seed (same bucket draws) for all,
+    on this process group.  Plans that need a cost model use rank 0's calibration sweep of the
+    block on this GPU, broadcast so every rank builds the same plan."""
     from .catalogs import reference_default_catalog
+    from .costfit import CostModel, QuadraticCostModel
     from .scheduler import DualConstraint, TokenBudget
 
     dev = torch.device("cuda", local)
     catalog, weights, tb, dc = reference_default_catalog()
-    # the reference's defaults (480k-token envelope, M_comp = 3e9, p = 2: cluster_sim.py:328-336);
-    # a different token budget scales M_comp to keep the reference's M_comp / M_mem^2
     m_mem = token_budget
+    # a different token budget scales M_comp to keep the reference's M_comp / M_mem^2
     m_comp = m_comp or dc.m_comp * (m_mem / dc.m_mem) ** 2
-    plan_a = emit_plan(catalog, TokenBudget(m_mem))
-    plan_b = emit_plan(catalog, DualConstraint(float(m_mem), m_comp, 2.0))
+    plans = {"equal_token": emit_plan(catalog, TokenBudget(m_mem)),
+             "dual_reference": emit_plan(catalog, DualConstraint(float(m_mem), m_comp, 2.0))}
     calib = None
-    if plan_kind == "calibrated":
-        from .costfit import CostModel, QuadraticCostModel
-
+    if any(a in ("dual_power_fit", "dual_quadratic") for a in arms):
         vec = torch.zeros(8, dtype=torch.float64, device=dev)
         trials = []
         if rank == 0:
@@ -398,50 +417,142 @@ def run_ab(world: int, rank: int, local: int, steps: int, warmup: int, seed: int
             dist.broadcast(vec, 0)
         v = [float(a) for a in vec.cpu()]
         fits = {"power": CostModel(*v[:4]), "quadratic": QuadraticCostModel(*v[4:])}
-        plan_b = plan_from_fit(cost_model, fits[cost_model], catalog, m_mem)
-        calib = {"cost_model": cost_model,
-                 "power_fit": fits["power"].__dict__, "quadratic_fit": fits["quadratic"].__dict__,
+        plans["dual_power_fit"] = plan_from_fit("power", fits["power"], catalog, m_mem)
+        plans["dual_quadratic"] = plan_from_fit("quadratic", fits["quadratic"], catalog, m_mem)
+        calib = {"power_fit": fits["power"].__dict__, "quadratic_fit": fits["quadratic"].__dict__,
                  "trials": [[t.batch, t.seq_len, round(t.step_time, 6)] for t in trials],
-                 "predicted_ms": [round(1e3 * fits[cost_model].predict(e.batch_size,
-                                                                       e.bucket.seq_len), 3)
-                                  for e in plan_b.entries]}
-    out = {}
-    for name, plan in (("equal_token", plan_a), ("dual", plan_b)):
+                 "predicted_ms": {k: [round(1e3 * fits[k].predict(e.batch_size, e.bucket.seq_len), 3)
+                                      for e in plans[f"dual_{'power_fit' if k == 'power' else k}"].entries]
+                                  for k in ("power", "quadratic")}}
+    out, all_stats = {}, {}
+    for name in arms:
+        plan = plans[name]
         torch.manual_seed(0)
         runner = DPStepRunner(WanStyleBlock(), dev, world, rank, seed=seed)
         sampler = BucketSampler(catalog, weights, plan, max(world, 1), seed)
         warm_buckets(runner, plan)
         stats = run_policy_steps(runner, sampler, steps, warmup=warmup)
         out[name] = summarize(stats, world)
+        out[name]["plan"] = plan.batch_sizes()
         if not detail:
             out[name].pop("per_step", None)
+        if keep_stats:
+            all_stats[name] = stats
         del runner
         torch.cuda.empty_cache()
-    return {
+    base = out.get("equal_token")
+    res = {
         "config": {"workload": "Wan-2.1-1.3B-style block (D=1536, 12 heads, FFN 8960), fused "
                                "AdaLN x2, reference default catalog, per-rank draws",
-                   "token_budget": m_mem, "plan": plan_kind,
-                   "plan_equal_token": plan_a.batch_sizes(), "plan_dual": plan_b.batch_sizes(),
-                   "parallelism": f"dp{world}, one NCCL all-reduce per step", "steps": steps},
+                   "token_budget": m_mem, "m_comp_reference": m_comp,
+                   "arms": {a: ARM_DOC[a] for a in arms},
+                   "plans": {a: plans[a].batch_sizes() for a in arms},
+                   "parallelism": f"dp{world}, one NCCL all-reduce per step", "steps": steps,
+                   "seed": seed},
         "policies": out,
         "calibration": calib,
-        "imbalance": {
-            "compute_cv_equal_token_pct": out["equal_token"]["mean_compute_cv"],
-            "compute_cv_dual_pct": out["dual"]["mean_compute_cv"],
-            "cv_step_measured_equal_token": out["equal_token"]["mean_cv_step_measured"],
-            "cv_step_measured_dual": out["dual"]["mean_cv_step_measured"],
-            "wait_sync_ms_equal_token": out["equal_token"]["mean_wait_sync_ms"],
-            "wait_sync_ms_dual": out["dual"]["mean_wait_sync_ms"],
-        },
-        "throughput_gain_vs_equal_token": (out["dual"]["tokens_per_sec"]
-                                           / max(out["equal_token"]["tokens_per_sec"], 1e-9)
-                                           - 1.0),
+        "imbalance": {a: {"compute_cv_pct": out[a]["mean_compute_cv"],
+                          "cv_step_measured": out[a]["mean_cv_step_measured"],
+                          "wait_sync_ms": out[a]["mean_wait_sync_ms"],
+                          "tokens_per_sec": out[a]["tokens_per_sec"],
+                          "throughput_vs_equal_token": (None if base is None else
+                                                        out[a]["tokens_per_sec"]
+                                                        / max(base["tokens_per_sec"], 1e-9) - 1.0)}
+                      for a in arms},
     }
+    if keep_stats:
+        res["_stats"] = all_stats
+        res["_plans"] = {a: plans[a] for a in arms}
+    return res
+
+
+def run_ab(world: int, rank: int, local: int, steps: int, warmup: int, seed: int = 42,
+           token_budget: int = 480_000, m_comp: float = 0.0, plan_kind: str = "calibrated",
+           cost_model: str = "quadratic", detail: bool = True) -> dict:
+    """Two-arm form (equal token vs one dual plan) kept for the earlier tools: the dual arm is
+    the calibrated plan of `cost_model` or, with plan_kind="reference", the reference's."""
+    dual = ("dual_reference" if plan_kind == "reference" else
+            "dual_power_fit" if cost_model == "power" else "dual_quadratic")
+    r = run_arms(world, rank, local, steps, warmup, seed, token_budget, m_comp,
+                 ("equal_token", dual), detail)
+    pol = {"equal_token": r["policies"]["equal_token"], "dual": r["policies"][dual]}
+    r["policies"] = pol
+    r["config"]["plan_equal_token"] = pol["equal_token"]["plan"]
+    r["config"]["plan_dual"] = pol["dual"]["plan"]
+    r["imbalance"] = {
+        "compute_cv_equal_token_pct": pol["equal_token"]["mean_compute_cv"],
+        "compute_cv_dual_pct": pol["dual"]["mean_compute_cv"],
+        "cv_step_measured_equal_token": pol["equal_token"]["mean_cv_step_measured"],
+        "cv_step_measured_dual": pol["dual"]["mean_cv_step_measured"],
+        "wait_sync_ms_equal_token": pol["equal_token"]["mean_wait_sync_ms"],
+        "wait_sync_ms_dual": pol["dual"]["mean_wait_sync_ms"],
+    }
+    r["throughput_gain_vs_equal_token"] = (pol["dual"]["tokens_per_sec"]
+                                           / max(pol["equal_token"]["tokens_per_sec"], 1e-9) - 1.0)
+    if r.get("calibration"):
+        key = "power" if dual == "dual_power_fit" else "quadratic"
+        r["calibration"]["cost_model"] = key
+        r["calibration"]["predicted_ms"] = r["calibration"]["predicted_ms"].get(key)
+    return r
+
+
+def write_traces(trace_dir, res: dict, world: int, command: str) -> dict:
+    """The measured steps in the reference's file formats, one set per arm:
+    trial trace JSONL (B_i, S_i, T_i per rank and step -- what the reference CLI's `fit`
+    consumes) with a manifest sidecar, plan JSON, the fitted models, per-step metrics CSV
+    (t_sync, cv_step, compute_cv, tokens/s, theta) and a summary JSON, all with manifests."""
+    from pathlib import Path
+
+    from .costfit import CostModel
+    from .manifest import make_manifest
+    from .sampler import latent_units
+    from .shapes import LatentGeometry
+    from .traces import (save_metrics_csv, save_model, save_plan, save_summary, save_trace,
+                         trials_from_steps, write_manifest_sidecar)
+
+    d = Path(trace_dir)
+    d.mkdir(parents=True, exist_ok=True)
+    cfg = res["config"]
+    written, rows = {}, {}
+    geom = LatentGeometry()
+    for arm, stats in res["_stats"].items():
+        trials, workers = trials_from_steps(stats)
+        tr = d / f"trace_{arm}.jsonl"
+        save_trace(tr, trials, workers)
+        man = make_manifest(command, {**cfg, "arm": arm}, [], [tr.name], cfg["seed"])
+        write_manifest_sidecar(tr, man)
+        pl = d / f"plan_{arm}.json"
+        save_plan(pl, res["_plans"][arm], make_manifest(command, {**cfg, "arm": arm}, [],
+                                                         [pl.name], cfg["seed"]))
+        rows[arm] = []
+        for st in stats:
+            t_sync = max(st.t_compute_ms) / 1e3
+            units = sum(latent_units(sh, geom) for sh in st.shards)
+            rows[arm].append({"t_sync": t_sync, "cv_step": st.cv_step,
+                              "compute_cv": st.compute_cv, "tokens_per_sec": st.tokens / t_sync,
+                              "theta": units / t_sync})
+        written[arm] = [tr.name, tr.name + ".manifest.json", pl.name]
+    mc = d / "metrics.csv"
+    save_metrics_csv(mc, rows)
+    write_manifest_sidecar(mc, make_manifest(command, cfg, [], [mc.name], cfg["seed"]))
+    if res.get("calibration"):
+        pf = res["calibration"]["power_fit"]
+        save_model(d / "model_power_fit.json", CostModel(pf["a"], pf["b"], pf["p"], pf["r2"]),
+                   make_manifest(command, cfg, [], ["model_power_fit.json"], cfg["seed"]))
+    summ = {k: v for k, v in res.items() if not k.startswith("_")}
+    for pol in summ["policies"].values():
+        pol.pop("per_step", None)
+    save_summary(d / "summary.json", {"world": world, **summ},
+                 make_manifest(command, cfg, [], ["summary.json"], cfg["seed"]))
+    return {"dir": str(d), "files": sorted(p.name for p in d.iterdir())}
 
 
 def bench_main(args, rest, world: int, rank: int, local: int) -> None:
-    """``bench.py --workload dit``: tokens/s of the balanced step at N GPUs (dual-constraint
-    plan) next to the equal-token baseline, with measured and load imbalance."""
+    """``bench.py --workload dit``: tokens/s of the DiT-block DP step at N GPUs under each bucket
+    plan (ARMS: equal token, the reference's dual constraint, the reference fitter's power-law
+    dual on B200 trials, the two-term time-balanced plan), same draws for every arm, with the
+    measured per-rank imbalance.  ``value`` is the time-balanced arm's tokens/s.
+    ``--trace-dir DIR`` writes the measured steps in the reference's file formats."""
     import argparse
 
     ap = argparse.ArgumentParser()
@@ -449,20 +560,28 @@ def bench_main(args, rest, world: int, rank: int, local: int) -> None:
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--token-budget", type=int, default=480_000)
     ap.add_argument("--m-comp", type=float, default=0.0)
-    ap.add_argument("--plan", choices=["calibrated", "reference"], default="calibrated")
-    ap.add_argument("--cost-model", choices=["quadratic", "power"], default="quadratic")
+    ap.add_argument("--arms", default=",".join(ARMS))
+    ap.add_argument("--trace-dir", default="")
     extra = ap.parse_args(rest)
     steps = extra.policy_steps or args.steps
-    res = run_ab(world, rank, local, steps, args.warmup, extra.seed, extra.token_budget,
-                 extra.m_comp, extra.plan, extra.cost_model)
+    arms = tuple(a for a in extra.arms.split(",") if a)
+    bad = [a for a in arms if a not in ARMS]
+    if bad:
+        raise SystemExit(f"unknown arm(s) {bad}; choose from {ARMS}")
+    res = run_arms(world, rank, local, steps, args.warmup, extra.seed, extra.token_budget,
+                   extra.m_comp, arms, detail=True, keep_stats=bool(extra.trace_dir))
     if rank == 0:
-        dual = res["policies"]["dual"]
+        head = "dual_quadratic" if "dual_quadratic" in arms else arms[-1]
+        pol = res["policies"][head]
+        if extra.trace_dir:
+            res["traces"] = write_traces(extra.trace_dir, res, world,
+                                         f"bench.py --workload dit --gpus {world}")
         line = {
             "metric": "DiT-block DP step tokens/s (dual-constraint buckets)",
-            "value": round(dual["tokens_per_sec"], 1), "unit": "tokens/s",
+            "value": round(pol["tokens_per_sec"], 1), "unit": "tokens/s", "arm": head,
             "n_gpus": world, "steps": steps, "warmup": args.warmup,
-            "ms_per_step": round(dual["mean_step_ms"], 3), "higher_is_better": True,
+            "ms_per_step": round(pol["mean_step_ms"], 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            **res,
+            **{k: v for k, v in res.items() if not k.startswith("_")},
         }
         print(json.dumps(line), flush=True)

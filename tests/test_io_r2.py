@@ -112,3 +112,37 @@ def test_adaptiveload_drop_in_import_path():
     assert scheduler.emit_plan(cat, default_dual_constraint()).batch_sizes() == [300, 100, 32, 5, 1, 1]
     assert shapes.sequence_length(shapes.MediaShape(81, 480, 832),
                                   shapes.LatentGeometry(temporal_factor=4)) == 32760
+
+
+def test_dp_step_trace_writer(tmp_path):
+    """bench.py --workload dit --trace-dir: measured DP steps in the reference formats."""
+    from paper_2605_17923_b200.dp_step import StepStats, summarize, write_traces
+    from paper_2605_17923_b200.sampler import RankShard
+    from paper_2605_17923_b200.scheduler import TokenBudget, emit_plan
+
+    cat, w, tb, dc = reference_default_catalog()
+    plan = emit_plan(cat, tb)
+    stats = []
+    for i in range(3):
+        shards = [RankShard(r, k, cat[k], plan.entries[k].batch_size) for r, k in enumerate((0, 3))]
+        t = [100.0 + 10 * i, 140.0]
+        stats.append(StepStats(i, shards, t, 150.0, sum(s.tokens for s in shards),
+                               [s.load for s in shards], 1 - t[0] / t[1], 50.0,
+                               [max(t) - v for v in t]))
+    res = {"config": {"seed": 42, "workload": "unit"}, "calibration": None,
+           "policies": {"equal_token": summarize(stats, 2)},
+           "_stats": {"equal_token": stats}, "_plans": {"equal_token": plan}}
+    out = write_traces(tmp_path, res, 2, "unit-test")
+    assert {"trace_equal_token.jsonl", "trace_equal_token.jsonl.manifest.json",
+            "plan_equal_token.json", "metrics.csv", "metrics.csv.manifest.json",
+            "summary.json"} <= set(out["files"])
+    trials = traces.load_trace(tmp_path / "trace_equal_token.jsonl")
+    assert [(t.batch, t.seq_len) for t in trials[:2]] == [(plan.entries[0].batch_size, cat[0].seq_len),
+                                                         (plan.entries[3].batch_size, cat[3].seq_len)]
+    assert trials[1].step_time == 0.14
+    assert traces.load_plan(tmp_path / "plan_equal_token.json").batch_sizes() == plan.batch_sizes()
+    head = (tmp_path / "metrics.csv").read_text().splitlines()[0]
+    assert head == ",".join(traces.METRICS_COLUMNS)
+    summ = json.loads((tmp_path / "summary.json").read_text())
+    assert summ["policies"]["equal_token"]["bottleneck"]["straggler_fraction"] == [0.0, 1.0]
+    assert len(summ["manifest"]["config_digest"]) == 64
