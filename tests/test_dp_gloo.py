@@ -137,3 +137,44 @@ def test_closed_loop_refit_agrees_across_ranks(gloo_results):
     a, b = gloo_results[0]["refit"], gloo_results[1]["refit"]
     assert len(a) == 2 and a == b
     assert all("plan" in e or "error" in e for e in a)
+
+
+# ------------------------------------------------------------------ world size 8 (one B200 box)
+def _worker8(rank, world, port, outdir):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    from paper_2605_17923_b200.costfit import analyze_bottleneck
+    from paper_2605_17923_b200.dp_step import run_policy_steps, summarize
+
+    torch.manual_seed(0)
+    runner = DPStepRunner(WanStyleBlock(CFG, norm_fn=cpu_adaln), torch.device("cpu"), world, rank,
+                          dtype=torch.float32)
+    # CPU-sized batches: the bucket index picks a short sequence, the plan's B is kept small
+    runner.make_batch = lambda sh: batch_for(
+        RankShard(sh.rank, sh.bucket_index, type(sh.bucket)(sh.bucket.shape, 6 + 2 * sh.bucket_index, 1),
+                  1 + sh.bucket_index % 3), 11 + rank)
+    cat, w, tb, dc = reference_default_catalog()
+    sampler = BucketSampler(cat, w, emit_plan(cat, dc), world, 42)
+    stats = run_policy_steps(runner, sampler, 3, warmup=1)
+    summ = summarize(stats, world)
+    bn = analyze_bottleneck(stats)
+    torch.save({"grad": runner.flat_grad.clone(), "times": [s.t_compute_ms for s in stats],
+                "seq": [[sh.seq_len for sh in s.shards] for s in stats],
+                "straggler": bn.straggler_fraction, "steps": summ["steps"]},
+               os.path.join(outdir, f"rank{rank}.pt"))
+    dist.destroy_process_group()
+
+
+def test_world8_dp_step_host_logic(tmp_path):
+    """The 8-rank path the driver's scale run takes (host side, gloo): every rank sees the same
+    draws and the same all-gathered per-rank times, the one flat all-reduce leaves identical
+    gradients everywhere, and the bottleneck report has one entry per rank."""
+    world = 8
+    mp.spawn(_worker8, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    res = [torch.load(tmp_path / f"rank{r}.pt", weights_only=False) for r in range(world)]
+    for r in res[1:]:
+        assert torch.equal(r["grad"], res[0]["grad"])
+        assert r["times"] == res[0]["times"] and r["seq"] == res[0]["seq"]
+    assert res[0]["steps"] == 3 and all(len(t) == world for t in res[0]["times"])
+    assert len(res[0]["straggler"]) == world
+    assert abs(sum(res[0]["straggler"]) - 1.0) < 1e-9 or sum(res[0]["straggler"]) >= 1.0
