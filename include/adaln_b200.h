@@ -211,6 +211,10 @@ AL_API int al_debug_clock_probe(unsigned long long* out, unsigned int spin_ns, v
  * event record between two launches breaks) is measured as it runs.  NULL disables. */
 AL_API int al_debug_set_timestamps(unsigned long long* buf, int capacity);
 
+/* Diagnostics: chunks stolen so far by the deterministic work-stealing backward on protocol
+ * slot `device_slot` of the current device (cumulative over launches). */
+AL_API int al_debug_steal_count(int device_slot, unsigned int* out);
+
 #ifdef __cplusplus
 }
 #endif

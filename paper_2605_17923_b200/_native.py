@@ -72,6 +72,7 @@ _SIGNATURES = {
     "al_set_tuning": (ctypes.c_int, [ctypes.c_int] * 6),
     "al_debug_clock_probe": (ctypes.c_int, [_p, ctypes.c_uint, _p]),
     "al_debug_set_timestamps": (ctypes.c_int, [_p, ctypes.c_int]),
+    "al_debug_steal_count": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint)]),
     "al_describe_launch": (
         ctypes.c_int,
         [ctypes.c_int, _i64, _i64, _i64, _i64, ctypes.c_int, _i64, ctypes.POINTER(_i64)],
@@ -161,6 +162,13 @@ def set_timestamps(buf_ptr: int | None, capacity: int = 0) -> None:
     (al_debug_set_timestamps); None disables."""
     check(load().al_debug_set_timestamps(buf_ptr, capacity if buf_ptr else 0),
           "al_debug_set_timestamps")
+
+
+def steal_count(slot: int = 0) -> int:
+    """Chunks stolen so far on work-stealing protocol slot `slot` (al_debug_steal_count)."""
+    v = ctypes.c_uint(0)
+    check(load().al_debug_steal_count(slot, ctypes.byref(v)), "al_debug_steal_count")
+    return int(v.value)
 
 
 def describe_launch(kernel: int, batch: int, seq: int, dim: int, mod_stride: int, dtype: int,

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdlib>
+#include <cstddef>
 #include <cstdio>
 #include <mutex>
 #include <unordered_map>
@@ -230,7 +231,28 @@ const void* pipe_t(int R, bool full, bool dyn) {
 const void* pipe_kernel(int dtype, int V, int R, bool full, bool dyn) {
   if (V != 2 || (R != 1 && R != 2)) return nullptr;
   if (dtype == AL_BF16) return pipe_t<__nv_bfloat16, 2>(R, full, dyn);
+  if (dtype == AL_F16) return pipe_t<__half, 2>(R, full, dyn);
   return nullptr;
+}
+// deterministic work-stealing backward (adaln_bwd_steal, bwd_steal.cuh): R = 2 only
+template <typename T>
+const void* steal_t(int V, bool full, int threads = 384) {
+  if (V == 2 && threads <= 352)
+    return full ? (const void*)al::adaln_bwd_steal<T, 2, 2, true, 352>
+                : (const void*)al::adaln_bwd_steal<T, 2, 2, false, 352>;
+  switch (V) {
+    case 1: return full ? (const void*)al::adaln_bwd_steal<T, 1, 2, true> : (const void*)al::adaln_bwd_steal<T, 1, 2, false>;
+    case 2: return full ? (const void*)al::adaln_bwd_steal<T, 2, 2, true> : (const void*)al::adaln_bwd_steal<T, 2, 2, false>;
+    default: return full ? (const void*)al::adaln_bwd_steal<T, 4, 2, true> : (const void*)al::adaln_bwd_steal<T, 4, 2, false>;
+  }
+}
+const void* steal_kernel(int dtype, int V, bool full, int threads = 384) {
+  switch (dtype) {
+    case AL_BF16: return steal_t<__nv_bfloat16>(V, full, threads);
+    case AL_F16: return steal_t<__half>(V, full, threads);
+    case AL_F64: return steal_t<double>(V, full, threads);
+    default: return steal_t<float>(V, full, threads);
+  }
 }
 const void* rows_kernel(int dtype, int vi, bool repack) {
   return with_table(dtype, [&](const auto& t) {
@@ -765,6 +787,96 @@ unsigned int* sched_slot(int dev, cudaStream_t st) {
   return b + 2 * slot;
 }
 
+// Work-stealing protocol state (al::g_steal, bwd_steal.cuh), handed out like the ticket slots:
+// one per (device, stream) for eager launches, one never reused per captured launch.
+struct StealSlots {
+  std::mutex mu;
+  unsigned int next[64] = {};
+  std::unordered_map<uintptr_t, unsigned int> by_stream[64];
+};
+StealSlots g_steal_slots;
+
+al::StealSlot* steal_slot(int dev, cudaStream_t st) {
+  static std::atomic<al::StealSlot*> base[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  al::StealSlot* b = base[dev].load(std::memory_order_acquire);
+  if (b == nullptr) {
+    void* ptr = nullptr;
+    if (cudaGetSymbolAddress(&ptr, al::g_steal) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return nullptr;
+    }
+    b = static_cast<al::StealSlot*>(ptr);
+    base[dev].store(b, std::memory_order_release);
+  }
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_steal_slots.mu);
+  unsigned int slot;
+  if (cap == cudaStreamCaptureStatusNone) {
+    auto it = g_steal_slots.by_stream[dev].find(reinterpret_cast<uintptr_t>(st));
+    if (it != g_steal_slots.by_stream[dev].end()) {
+      slot = it->second;
+    } else {
+      if (g_steal_slots.next[dev] >= static_cast<unsigned int>(al::kStealSlots)) return nullptr;
+      slot = g_steal_slots.next[dev]++;
+      g_steal_slots.by_stream[dev].emplace(reinterpret_cast<uintptr_t>(st), slot);
+    }
+  } else {
+    if (g_steal_slots.next[dev] >= static_cast<unsigned int>(al::kStealSlots)) return nullptr;
+    slot = g_steal_slots.next[dev]++;
+  }
+  return b + slot;
+}
+
+// Backward load balancing: 1 (default) = deterministic work stealing (adaln_bwd_steal) for every
+// TMA-path launch it fits; 0 = the round-1 scheme (dynamic tail unless AL_BWD_DETERMINISTIC,
+// static otherwise).  AL_BWD_STEAL overrides for A/B runs.
+int bwd_steal_mode() {
+  static const int m = [] {
+    const char* v = std::getenv("AL_BWD_STEAL");
+    return v ? std::atoi(v) : 0;
+  }();
+  return m;
+}
+// rows per stealable chunk (AL_STEAL_CHUNK overrides; a multiple of the 2-row stage) and the
+// pool of stolen-chunk slots per launch in units of G (AL_STEAL_POOL; 0 disables stealing, the
+// chunked partition then runs statically)
+int steal_chunk_rows() {
+  static const int c = [] {
+    const char* v = std::getenv("AL_STEAL_CHUNK");
+    const int x = v ? std::atoi(v) : 8;
+    return x >= 2 ? (x + 1) / 2 * 2 : 8;
+  }();
+  return c;
+}
+int steal_pool_factor() {
+  static const int f = [] {
+    const char* v = std::getenv("AL_STEAL_POOL");
+    return v ? std::atoi(v) : 2;
+  }();
+  return f;
+}
+
+int64_t pipe_max_rows() {
+  static const int64_t m = [] {
+    const char* v = std::getenv("AL_BWD_PIPE_ROWS");
+    return v ? static_cast<int64_t>(std::atoll(v)) : int64_t(16384);
+  }();
+  return m;
+}
+
+int bwd_interleave() {
+  static const int m = [] {
+    const char* v = std::getenv("AL_BWD_INTERLEAVE");
+    return v ? std::atoi(v) : 1;
+  }();
+  return m;
+}
+
 // Fraction of the rows handed out dynamically by the 16-bit rows forward (the rest is a static
 // even split), capped at one modulation group.  Measured at cfg2 (bf16 D = 5 120, B200,
 // tools/bw_probe.py): forward 5 449 GB/s static, 5 699 / 6 004 / 6 093 / 6 110 / 6 174 GB/s
@@ -941,6 +1053,15 @@ __global__ void clock_probe_kernel(unsigned long long* out, unsigned int spin_ns
 
 extern "C" {
 
+int al_debug_steal_count(int device_slot, unsigned int* out) {
+  if (!out || device_slot < 0 || device_slot >= al::kStealSlots)
+    return fail(AL_ERR_VALUE, "bad slot or output");
+  cudaError_t e = cudaMemcpyFromSymbol(out, al::g_steal, sizeof(unsigned int),
+                                       device_slot * sizeof(al::StealSlot) +
+                                           offsetof(al::StealSlot, stolen));
+  return e == cudaSuccess ? AL_OK : cuda_fail(e, "cudaMemcpyFromSymbol");
+}
+
 int al_debug_set_timestamps(unsigned long long* buf, int capacity) {
   if (buf != nullptr && capacity <= 0) return fail(AL_ERR_VALUE, "capacity must be positive");
   g_ts_buf.store(nullptr, std::memory_order_release);
@@ -1000,6 +1121,11 @@ int al_device_init(int device) {
           for (bool full : {false, true}) {
             rc = ensure_attr(tma_kernel(kernel, dt, V, R, full), device);
             if (rc) return rc;
+            if (kernel == 1 && R == 2) {
+              rc = ensure_attr(steal_kernel(dt, V, full), device);
+              if (!rc) rc = ensure_attr(steal_kernel(dt, V, full, 352), device);
+              if (rc) return rc;
+            }
             if (kernel == 1 && tma_dyn_kernel(dt, V, R, full)) {
               rc = ensure_attr(tma_dyn_kernel(dt, V, R, full), device);
               if (rc) return rc;
@@ -1182,9 +1308,9 @@ int64_t al_adaln_backward_workspace_bytes(int64_t batch, int64_t seq, int64_t di
   if (make_plan(1, N, dim, mod_stride, dtype, n_tile, aligned, 1, &pa)) return -1;
   if (make_plan(1, N, dim, mod_stride, dtype, n_tile, aligned, 1, &pg, true)) return -1;
   const int64_t ngroups = mod_stride ? batch : 1;
-  // static slots (G + groups - 1) + the dynamic tail's G slots; + 16 bytes: the fused stage-2
-  // grid-barrier counter
-  return 2 * (std::max(pa.grid, pg.grid) + ngroups - 1 + pa.grid) * dim * ct_size(dtype) + 16;
+  // static slots (G + groups - 1) + the larger of the dynamic tail's G slots and the work
+  // stealing pool (2G); + 16 bytes: the fused stage-2 grid-barrier counter
+  return 2 * (std::max(pa.grid, pg.grid) + ngroups - 1 + 2 * pa.grid) * dim * ct_size(dtype) + 16;
 }
 
 int al_adaln_backward(const void* dy, const void* x, const void* scale, const void* mean,
@@ -1228,8 +1354,17 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   // Dynamic tail (see adaln_bwd_tma): TMA path, vector stage 2, no explicit n_tile, not the
   // cooperative fused stage 2, caller did not ask for AL_BWD_DETERMINISTIC, and at least two
   // stages per CTA in the tail (which stays inside the last group).
+  // Short launches (<= pipe_max_rows() rows, ~100 rows per CTA at D = 5 120) take the
+  // skewed-pipeline kernel with its static partition: its barrier-free stages fill the few
+  // stages a CTA has faster (B200, device timestamps: S = 1 560 / 3 600 / 7 800 and B = 4, 8
+  // x 1 560: 7-9 % less time than the lock-step kernel; equal at 14 040; 3 % more at 32 760,
+  // profiles/r2_bwd_variants.jsonl).  Deterministic either way.
+  const bool pipe_auto = tu.variant == 0 && pl.path == 1 && vec && n_tile == 0 &&
+                         N <= pipe_max_rows() && pl.V == 2 &&
+                         (dtype == AL_BF16 || dtype == AL_F16);
   int64_t n_dyn = 0;
-  if (pl.path == 1 && vec && n_tile == 0 && tu.variant != 2 && !(flags & AL_BWD_DETERMINISTIC)) {
+  if (!pipe_auto && pl.path == 1 && vec && n_tile == 0 && tu.variant != 2 &&
+      !(flags & AL_BWD_DETERMINISTIC)) {
     const double f = bwd_dyn_frac();
     n_dyn = std::min<int64_t>(static_cast<int64_t>(static_cast<double>(N) * (f < 1.0 ? f : 1.0)),
                               S_grp);
@@ -1243,7 +1378,46 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
     const int64_t n_static = N - n_dyn;
     if (n_static > 0 && n_static < pl.grid) n_dyn = 0;
   }
-  const int64_t nslots = nslots_static + (n_dyn ? pl.grid : 0);
+  // Deterministic work stealing (bwd_steal.cuh): replaces both the dynamic tail and the plain
+  // static partition wherever it fits (TMA path with 2-row stages, vector stage 2, default
+  // tiling, >= 2 chunks per CTA); dscale/dshift are then bit-identical run to run whatever the
+  // caller's determinism flag.
+  bool use_steal = false;
+  al::StealSlot* sslot = nullptr;
+  const void* sfn = nullptr;
+  size_t steal_smem = 0;
+  // (tuning variant 4 = the round-1 scheme, for A/B runs)
+  if (bwd_steal_mode() == 1 && !pipe_auto && pl.path == 1 && vec && n_tile == 0 &&
+      tu.variant != 2 && tu.variant != 3 && tu.variant != 4 && pl.R == 2 && pl.grid <= al::kStealMaxG &&
+      N >= 2 * steal_chunk_rows() * static_cast<int64_t>(pl.grid)) {
+    const int nvec_ = static_cast<int>(dim * elem_size(dtype) / 16);
+    const bool full = pl.threads - 32 == nvec_ / pl.V && nvec_ % pl.V == 0;
+    sfn = steal_kernel(dtype, pl.V, full, pl.threads);
+    const int ncw = (pl.threads - 32) / 32;
+    const size_t stage = 2 * 2 * static_cast<size_t>(dim * elem_size(dtype));
+    // ring + barriers + headers + row-sum scratch + the [2][D] shared running total (the
+    // kernel's layout, bwd_steal.cuh)
+    auto r16 = [](size_t v) { return (v + 15) & ~size_t(15); };
+    auto extra = [&](int ns) {
+      return 16 * static_cast<size_t>(ns) + 24 * static_cast<size_t>(ns) +
+             r16(2 * static_cast<size_t>(ns) * 2 * cs) + r16(8 * static_cast<size_t>(ns) + 4) +
+             r16(2 * static_cast<size_t>(ncw) * 2 * 2 * cs) + 2 * static_cast<size_t>(dim) * cs;
+    };
+    int ns = pl.NS;
+    while (ns > 3 && ns * stage + extra(ns) > static_cast<size_t>(kSmemOptin)) --ns;
+    int dev;
+    if (ns * stage + extra(ns) <= static_cast<size_t>(kSmemOptin) && cudaGetDevice(&dev) == cudaSuccess && ensure_attr(sfn, dev) == AL_OK) {
+      sslot = steal_slot(dev, st);
+      if (sslot != nullptr) {
+        use_steal = true;
+        n_dyn = 0;
+        pl.NS = ns;
+        steal_smem = ns * stage + extra(ns);
+      }
+    }
+  }
+  const int64_t nslots = nslots_static + (use_steal ? steal_pool_factor() * pl.grid
+                                                    : (n_dyn ? pl.grid : 0));
   const int64_t need = 2 * nslots * dim * cs;
   if (!workspace || workspace_bytes < need) {
     return fail(AL_ERR_WORKSPACE, "workspace too small: need %lld bytes, got %lld",
@@ -1274,6 +1448,24 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   p.N_static = N;
   p.tail_slot0 = -1;
   p.ts = next_ts();
+  p.steal = nullptr;
+  p.chunk_rows = steal_chunk_rows();
+  p.pool_cap = 0;
+  p.interleave = 0;
+  if (use_steal) {
+    pl.fn = sfn;
+    pl.smem = steal_smem;
+    p.nstages = pl.NS;
+    p.steal = sslot;
+    p.pool_cap = steal_pool_factor() * pl.grid;
+    p.tail_slot0 = nslots_static;  // pool slots follow the static ones
+  }
+  // Interleaved static partition (single group): the static instance walks stages k, k+G, ...
+  // -- a fixed, deterministic assignment whose CTAs sweep HBM together (AL_BWD_INTERLEAVE=0
+  // restores the contiguous split)
+  if (!use_steal && !pipe_auto && n_dyn == 0 && pl.path == 1 && vec && tu.variant != 2 &&
+      tu.variant != 3 && S_grp == N && bwd_interleave())
+    p.interleave = 1;
   if (n_dyn) {
     int dev;
     const bool full = pl.threads - 32 == p.nvec / pl.V && p.nvec % pl.V == 0;
@@ -1290,7 +1482,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   }
   // Skewed-pipeline stage 1 (variant 3 while under evaluation): same ring/slot contract, its
   // own ring depth (the consumers hold two slots at a time)
-  if (pl.path == 1 && tu.variant == 3) {
+  if (pl.path == 1 && (tu.variant == 3 || pipe_auto)) {
     const int R = tu.R ? tu.R : 2;
     const bool full = pl.threads - 32 == p.nvec / pl.V && p.nvec % pl.V == 0;
     const void* fn = pipe_kernel(dtype, pl.V, R, full, p.sched != nullptr);
@@ -1301,7 +1493,9 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
         return static_cast<size_t>(2 * ns + 4) * 8 + 4 * ncw * 2 * R * cs + 16 +
                static_cast<size_t>(ns) * (8 + 4 + 2 * R * cs) + 32;
       };
-      const size_t budget = tu.smem_budget ? static_cast<size_t>(tu.smem_budget) : 210 * 1024;
+      // the ring plan's per-CTA shared memory, so the occupancy (and the grid the slots were
+      // sized for) is unchanged
+      const size_t budget = tu.smem_budget ? static_cast<size_t>(tu.smem_budget) : pl.smem;
       int ns = 2;
       while (ns < 12 && (ns + 1) * stage + extra(ns + 1) <= budget) ++ns;
       int dev;
@@ -1335,8 +1529,9 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   // stage 2: 16-byte vector form when every partial row is 16-byte aligned
   const void* rk = reduce_kernel(dtype, vec);
   int64_t G64 = pl.grid;
-  void* rargs[] = {&workspace, &dscale, &dshift,     &p.N,           &p.S_grp, &p.D,
-                   &G64,       &p.nslots, &p.N_static, &p.tail_slot0, &p.ts};
+  int64_t k3_tail0 = use_steal ? -1 : p.tail_slot0;  // stolen partials are merged by owners
+  void* rargs[] = {&workspace, &dscale, &dshift,     &p.N,      &p.S_grp, &p.D,
+                   &G64,       &p.nslots, &p.N_static, &k3_tail0, &p.ts};
   const int64_t cols_per_cta = vec ? al::kRedCV * (16 / cs) : 32;
   dim3 rgrid(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
              static_cast<unsigned>(ngroups));

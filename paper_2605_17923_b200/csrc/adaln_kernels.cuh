@@ -69,6 +69,8 @@ struct FwdParams {
 constexpr int kSchedSlots = 16384;
 __device__ unsigned int g_sched[kSchedSlots][2];
 
+struct StealSlot;  // bwd_steal.cuh
+
 struct BwdParams {
   const void* dy;
   const void* x;
@@ -99,6 +101,13 @@ struct BwdParams {
   int64_t N_static;
   int64_t tail_slot0;
   unsigned long long* ts;  // nullable: start stamped here, end by the stage-2 kernel
+  // deterministic work stealing (adaln_bwd_steal): protocol state, rows per chunk, pool slots
+  // (stolen-chunk partials live in slots tail_slot0 + [0, pool_cap))
+  StealSlot* steal;
+  int chunk_rows;
+  int pool_cap;
+  // interleaved static partition (single group, adaln_bwd_tma static instance)
+  int interleave;
 };
 
 // Row partition shared by stage 1 and stage 2.
@@ -113,16 +122,37 @@ __host__ __device__ __forceinline__ int64_t part_owner(int64_t row, int64_t N, i
 // Stage schedule walker: stages of at most R rows, never crossing a group boundary.
 struct StageWalker {
   int64_t row, r1, gend, grp, S;
+  int64_t step = 0;  // > 0: interleaved single-group walk (init_interleaved)
   __device__ __forceinline__ void init(int64_t r0, int64_t r1_, int64_t S_) {
     row = r0;
     r1 = r1_;
     S = S_;
     grp = r0 / S_;
     gend = (grp + 1) * S_;
+    step = 0;
+  }
+  // Interleaved partition of a single group: CTA k takes stages k, k + G, k + 2G, ... (R rows
+  // each), so at any moment all CTAs stream neighbouring rows -- one sequential sweep through
+  // HBM instead of G scattered streams -- while the assignment stays fixed (deterministic).
+  __device__ __forceinline__ void init_interleaved(int64_t k, int64_t G, int64_t N, int R) {
+    row = k * R;
+    r1 = N;
+    S = N;
+    grp = 0;
+    gend = N;
+    step = G * R;
   }
   __device__ __forceinline__ bool done() const { return row >= r1; }
   // Rows of the next stage (call only when !done()); advances past it.
   __device__ __forceinline__ int next(int R, int64_t& start, int64_t& g) {
+    if (step) {
+      const int64_t left = r1 - row;
+      const int n = left < R ? static_cast<int>(left) : R;
+      start = row;
+      g = 0;
+      row += step;
+      return n;
+    }
     if (row >= gend) {
       ++grp;
       gend += S;
@@ -1363,7 +1393,8 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       const uint8_t* xb = static_cast<const uint8_t*>(p.x);
       const uint8_t* db = static_cast<const uint8_t*>(p.dy);
       StageWalker w;
-      w.init(r0, r1, p.S_grp);
+      if (!DYN && p.interleave) w.init_interleaved(k, p.G, p.N, R);
+      else w.init(r0, r1, p.S_grp);
       int s = 0;
       uint32_t f = 0;
       auto issue = [&](int64_t start, int rows) {
@@ -1657,7 +1688,8 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
     // (cfg2: 5 870 vs 5 087 GB/s).
   int64_t cur_g = -1;
   StageWalker w;
-  w.init(r0, r1, p.S_grp);
+  if (p.interleave) w.init_interleaved(k, p.G, p.N, R);
+  else w.init(r0, r1, p.S_grp);
   int s = 0;
   uint32_t ph = 0;
   int it = 0;
@@ -1807,6 +1839,7 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
     }
   }
   if (cur_g >= 0) flush(k + cur_g);
+  else if (p.interleave) flush(k);  // no stage for this CTA: its slot still takes part (zeros)
   }
 #ifdef AL_CTA_TRACE
   named_bar_sync(1, nc);
@@ -1893,7 +1926,8 @@ __global__ void __launch_bounds__(384, 1) adaln_bwd_pipe(const BwdParams p) {
       const uint8_t* xb = static_cast<const uint8_t*>(p.x);
       const uint8_t* db = static_cast<const uint8_t*>(p.dy);
       StageWalker w;
-      w.init(r0, r1, p.S_grp);
+      if (!DYN && p.interleave) w.init_interleaved(k, p.G, p.N, R);
+      else w.init(r0, r1, p.S_grp);
       int s = 0;
       uint32_t f = 0;
       auto issue = [&](int64_t start, int rows) {
@@ -2089,10 +2123,10 @@ __global__ void __launch_bounds__(384, 1) adaln_bwd_pipe(const BwdParams p) {
         const CT rr_ = pd.r[rr];
         const CT c0 = -rr_ * tot[2 * rr] * invD, c1 = -rr_ * tot[2 * rr + 1] * invD;
         const P r2 = splat2(rr_);
-        // 16-bit: dx = g*r + (x*(c1*r) + (c0 - c1*m*r)), xhat folded into the constants;
-        // 32/64-bit: xhat recomputed exactly as in phase 1, dx = g*r + (xhat*c1 + c0)
-        const P a1 = splat2(c1 * rr_), a0 = splat2(c0 - c1 * pd.m[rr] * rr_);
+        // xhat and g recomputed exactly as in phase 1 (and as adaln_bwd_tma keeps them), then
+        // dx = g*r + (xhat*c1 + c0): dx is bit-identical to the lock-step kernel's
         const P nm = splat2(-pd.m[rr]), pc1 = splat2(c1), pc0 = splat2(c0);
+        const P nmr = splat2(-pd.m[rr] * rr_);
 #pragma unroll
         for (int j = 0; j < V; ++j) {
           if (vmask >> j & 1) {
@@ -2103,12 +2137,10 @@ __global__ void __launch_bounds__(384, 1) adaln_bwd_pipe(const BwdParams p) {
 #pragma unroll
             for (int e = 0; e < NP; ++e) {
               const P gg = mul2(dv[e], s1[j][e]);
-              if constexpr (sizeof(T) == 2) {
-                o[e] = fma2(gg, r2, fma2(xv[e], a1, a0));
-              } else {
-                const P xh = mul2(add2(xv[e], nm), r2);
-                o[e] = fma2(gg, r2, fma2(xh, pc1, pc0));
-              }
+              P xh;
+              if constexpr (sizeof(T) == 2) xh = fma2(xv[e], r2, nmr);
+              else xh = mul2(add2(xv[e], nm), r2);
+              o[e] = fma2(gg, r2, fma2(xh, pc1, pc0));
             }
             st_global_cs(dxrow + rr * RB + coff[j], pack2<T>(o));
           }
@@ -2512,3 +2544,6 @@ __global__ void __launch_bounds__(256) adaln_bwd_generic(const BwdParams p) {
 }
 
 }  // namespace al
+
+#include "bwd_steal.cuh"
+

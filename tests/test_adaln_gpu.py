@@ -342,8 +342,11 @@ def test_dynamic_tail_backward(shape, mod, cuda):
             torch.float64: nat.AL_F64}[dt]
     plan = nat.describe_launch(1, b, s_, d, 0 if len(shape) == 2 else d, code)
     s_last = b * s_ if len(shape) == 2 else s_
+    # short 16-bit launches (<= 16 384 rows) take the skewed-pipeline kernel, statically
+    pipe = (dt in (torch.bfloat16, torch.float16) and b * s_ <= 16384
+            and plan["vecs_per_thread"] == 2)
     dynamic = (plan["path"] == "tma" and plan["rows_per_stage"] in (2, 4)
-               and s_last >= 64 * plan["grid"])
+               and s_last >= 64 * plan["grid"] and not pipe)
     assert torch.equal(got[1], ref[1]) != dynamic, plan
     h = lambda t: t.double().cpu().numpy()  # noqa: E731
     if len(shape) == 3:

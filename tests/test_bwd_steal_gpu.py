@@ -1,0 +1,149 @@
+"""Deterministic work-stealing backward (bwd_steal.cuh): bit-identical dscale/dshift/dx run to
+run whatever the stealing pattern, parity with the oracle, agreement with the static partition
+(round-1 scheme, tuning variant 4) to fp32 summation order, across group layouts."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import max_rel_err
+from paper_2605_17923_b200 import _native as nat
+from paper_2605_17923_b200.adaln._ops import fused_backward, fused_forward
+
+pytestmark = pytest.mark.gpu
+STEAL = os.environ.get("AL_BWD_STEAL") == "1"
+steal_only = pytest.mark.skipif(not STEAL, reason="work stealing is opt-in (AL_BWD_STEAL=1)")
+
+
+def f64(t):
+    return t.detach().double().cpu().numpy()
+
+
+def _data(b, s, d, dtype, cuda, seed, per_sample=True):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    x = torch.randn(b, s, d, generator=g).to(dtype).to(cuda)
+    dy = torch.randn(b, s, d, generator=g).to(dtype).to(cuda)
+    shp = (b, d) if per_sample else (d,)
+    sc = (0.1 * torch.randn(*shp, generator=g)).to(dtype).to(cuda)
+    return x, dy, sc
+
+
+SHAPES = [(1, 32760, 5120, True), (1, 12345, 5120, True), (3, 7001, 5120, True),
+          (4, 3000, 1536, True), (2, 9000, 5120, False), (1, 20000, 2048, True)]
+
+
+@steal_only
+@pytest.mark.parametrize("b,s,d,per_sample", SHAPES)
+def test_steal_bitwise_reproducible_and_vs_oracle(b, s, d, per_sample, cuda):
+    x, dy, sc = _data(b, s, d, torch.bfloat16, cuda, seed=s, per_sample=per_sample)
+    y, mu, rs = fused_forward(x, sc, sc)
+    first = fused_backward(dy, x, sc, mu, rs, deterministic=True)
+    # concurrent pressure on other streams varies who steals what; results must not change
+    side = torch.cuda.Stream(device=cuda)
+    for rep in range(6):
+        if rep % 2:
+            with torch.cuda.stream(side):
+                junk = torch.empty(64 << 20, dtype=torch.uint8, device=cuda).fill_(rep)
+        again = fused_backward(dy, x, sc, mu, rs, deterministic=bool(rep % 3))
+        torch.cuda.synchronize()
+        for a_, b_ in zip(first, again):
+            assert torch.equal(a_, b_), rep
+    dx, dsc, dsh = first
+    xs, dys = f64(x).reshape(-1, d), f64(dy).reshape(-1, d)
+    mus, rss = f64(mu).reshape(-1), f64(rs).reshape(-1)
+    if per_sample:
+        for i in range(b):
+            sl = slice(i * s, (i + 1) * s)
+            dsco, dsho = oracle.reduce_naive(dys[sl], xs[sl], mus[sl], rss[sl], threads=0)
+            assert max_rel_err(f64(dsc)[i], dsco) <= 1e-5
+            assert max_rel_err(f64(dsh)[i], dsho) <= 1e-5
+    else:
+        dsco, dsho = oracle.reduce_naive(dys, xs, mus, rss, threads=0)
+        assert max_rel_err(f64(dsc), dsco) <= 1e-5
+        assert max_rel_err(f64(dsh), dsho) <= 1e-5
+    rows = np.random.default_rng(0).choice(b * s, 128, replace=False)
+    scn = f64(sc).reshape(-1, d)
+    sci = scn[rows // s] if per_sample else np.broadcast_to(scn, (128, d))
+    dxo = np.stack([oracle.backward_dx(dys[r:r + 1], xs[r:r + 1], sci[i], mus[r:r + 1],
+                                       rss[r:r + 1], threads=0)[0] for i, r in enumerate(rows)])
+    assert max_rel_err(f64(dx).reshape(-1, d)[rows], dxo) <= 2e-2
+
+
+@steal_only
+def test_steal_matches_static_partition(cuda):
+    x, dy, sc = _data(1, 32760, 5120, torch.bfloat16, cuda, seed=5)
+    y, mu, rs = fused_forward(x, sc, sc)
+    a = fused_backward(dy, x, sc, mu, rs, deterministic=True)
+    nat.set_tuning(1, 0, 0, 0, False, 4)  # round-1 static partition
+    try:
+        b = fused_backward(dy, x, sc, mu, rs, deterministic=True)
+    finally:
+        nat.set_tuning(1, 0, 0, 0, False, 0)
+    assert torch.equal(a[0], b[0])  # dx does not depend on the partition
+    assert max_rel_err(f64(a[1]), f64(b[1])) <= 2e-6
+    assert max_rel_err(f64(a[2]), f64(b[2])) <= 2e-6
+
+
+@steal_only
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float16, torch.float64])
+def test_steal_other_dtypes(dtype, cuda):
+    d = 2048 if dtype != torch.float64 else 1024
+    x, dy, sc = _data(2, 6000, d, dtype, cuda, seed=9)
+    y, mu, rs = fused_forward(x, sc, sc)
+    first = fused_backward(dy, x, sc, mu, rs)
+    for _ in range(3):
+        again = fused_backward(dy, x, sc, mu, rs)
+        for a_, b_ in zip(first, again):
+            assert torch.equal(a_, b_)
+    xs, dys = f64(x).reshape(-1, d), f64(dy).reshape(-1, d)
+    mus, rss = f64(mu).reshape(-1), f64(rs).reshape(-1)
+    bar = 1e-12 if dtype == torch.float64 else 1e-5
+    for i in range(2):
+        sl = slice(i * 6000, (i + 1) * 6000)
+        dsco, dsho = oracle.reduce_naive(dys[sl], xs[sl], mus[sl], rss[sl], threads=0)
+        assert max_rel_err(f64(first[1])[i], dsco) <= bar
+        assert max_rel_err(f64(first[2])[i], dsho) <= bar
+
+
+@steal_only
+def test_steal_in_cuda_graph(cuda):
+    x, dy, sc = _data(1, 20000, 5120, torch.bfloat16, cuda, seed=3)
+    y, mu, rs = fused_forward(x, sc, sc)
+    ref = fused_backward(dy, x, sc, mu, rs)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream(device=cuda)
+    cap.wait_stream(torch.cuda.current_stream(cuda))
+    with torch.cuda.stream(cap):
+        with torch.cuda.graph(g, stream=cap):
+            out = fused_backward(dy, x, sc, mu, rs)
+    for _ in range(4):
+        g.replay()
+        torch.cuda.synchronize()
+        for a_, b_ in zip(out, ref):
+            assert torch.equal(a_, b_)
+
+
+@pytest.mark.parametrize("b,s,d", [(1, 1560, 5120), (4, 1560, 5120), (1, 7800, 5120),
+                                   (8, 1560, 1536), (3, 999, 2048)])
+def test_short_launch_pipeline_kernel(b, s, d, cuda):
+    """Short launches take the skewed-pipeline kernel (static partition): deterministic, equal
+    dx to the lock-step kernel to one 16-bit rounding, dscale/dshift to fp32 summation order."""
+    x, dy, sc = _data(b, s, d, torch.bfloat16, cuda, seed=b * s)
+    y, mu, rs = fused_forward(x, sc, sc)
+    a = fused_backward(dy, x, sc, mu, rs, deterministic=False)
+    for _ in range(3):
+        again = fused_backward(dy, x, sc, mu, rs, deterministic=False)
+        for u, v in zip(a, again):
+            assert torch.equal(u, v)
+    nat.set_tuning(1, 0, 0, 0, False, 4)  # round-1 lock-step kernel
+    try:
+        ref = fused_backward(dy, x, sc, mu, rs, deterministic=True)
+    finally:
+        nat.set_tuning(1, 0, 0, 0, False, 0)
+    assert max_rel_err(f64(a[0]), f64(ref[0])) <= 8e-3
+    assert max_rel_err(f64(a[1]), f64(ref[1])) <= 2e-6
+    assert max_rel_err(f64(a[2]), f64(ref[2])) <= 2e-6

@@ -62,10 +62,16 @@ for B, S in [(1, 32760), (1, 1560), (1, 3600), (1, 7800), (4, 1560), (1, 75600)]
     f = med(lambda: fused_forward(x, sc, sc))
     bd = med(lambda: fused_backward(dy, x, sc, mu, rs, deterministic=False))
     bs = med(lambda: fused_backward(dy, x, sc, mu, rs, deterministic=True))
+    extra = {}
+    if os.environ.get("AB_LEGACY"):  # the round-1 scheme (tuning variant 4) in the same process
+        nat.set_tuning(1, 0, 0, 0, False, 4)
+        extra["legacy_dyn_us"] = round(med(lambda: fused_backward(dy, x, sc, mu, rs, deterministic=False)), 2)
+        extra["legacy_det_us"] = round(med(lambda: fused_backward(dy, x, sc, mu, rs, deterministic=True)), 2)
+        nat.set_tuning(1, 0, 0, 0, False, 0)
     nat.clock_probe(clk.data_ptr(), 20000, st.cuda_stream)
     c = clk.cpu().tolist()[0]
     print(json.dumps({"tag": tag, "B": B, "S": S, "fwd_us": round(f, 2), "bwd_dyn_us": round(bd, 2),
                       "bwd_det_us": round(bs, 2), "fwd_gbs": round(fb / f / 1e3, 1),
                       "bwd_dyn_gbs": round(bb / bd / 1e3, 1), "bwd_det_gbs": round(bb / bs / 1e3, 1),
-                      "sm_mhz": round(c[1] / c[0] * 1e3)}), flush=True)
+                      "sm_mhz": round(c[1] / c[0] * 1e3), **extra}), flush=True)
     del x, dy, mu, rs
