@@ -395,11 +395,16 @@ def run_ours(args, world, rank, local):
         gr = adaln_backward_naive(dyh, xh, sch, out.mu, out.rstd, check_finite=False)
         return out, gr
 
-    # warm-up: the pinned host result buffers come from torch's caching host allocator; two
-    # generations are alive at once (previous step's results + this step's), so fill the cache
-    for _ in range(3):
+    # warm-up: the pinned host result buffers come from the host API's pinned pool; two
+    # generations are alive at once (previous step's results + this step's), so fill it; then
+    # one full collection, so a generational GC pass over the warm-up's garbage does not land
+    # inside the timed steps (tools/e2e_steps_diag.py: 95-170 ms steps 2-6 with GC, none without)
+    import gc
+
+    for _ in range(max(3, args.warmup)):
         out, gr = e2e_step()
     torch.cuda.synchronize(dev)
+    gc.collect()
     barrier(world)
     t0 = time.perf_counter()
     step_s = []
@@ -509,6 +514,7 @@ def run_ours(args, world, rank, local):
         "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "step_ms_min_max": [round(1e3 * min(step_s), 2), round(1e3 * max(step_s), 2)],
+                "step_ms_median": round(1e3 * statistics.median(step_s), 2),
                 "path": "adaln_forward + adaln_backward_naive on pinned torch CPU bf16 tensors"},
         "cpu_baseline": cpu,
         "gpu_launches": 3 * K,  # fwd K1 + bwd K2 + K3 per step (the deterministic leg is outside)

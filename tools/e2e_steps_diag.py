@@ -28,12 +28,15 @@ dyh = torch.randn(1, S, D).to(torch.bfloat16).pin_memory()
 sc = (0.1 * torch.randn(1, D)).to(torch.bfloat16).pin_memory()
 total = 5 * xh.numel() * 2 + 8 * S
 out = gr = None
-if "--no-gc" in sys.argv:
-    import gc
+import gc  # noqa: E402
 
+if "--no-gc" in sys.argv:
     gc.disable()
-for i in range(int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 12):
+COLLECT_AT = 3 if "--collect" in sys.argv else -1
+for i in range(int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 12):  # noqa: E501
     torch.cuda.synchronize()
+    if i == COLLECT_AT:
+        gc.collect()
     t = time.perf_counter()
     c = time.process_time()
     out = adaln_forward(xh, sc, sc, 1e-6, check_finite=False)
