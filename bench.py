@@ -547,8 +547,9 @@ def main():
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl == "ours":
         # NCCL communicator init lines (nRanks, NVLS / channels) for the driver's rank count;
         # NCCL reads these once, so they are set before anything imports torch
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        # (set, not setdefault: images that export NCCL_DEBUG=WARN would silence them)
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup(args)
     try:
