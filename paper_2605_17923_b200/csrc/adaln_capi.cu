@@ -1459,13 +1459,22 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
     p.steal = sslot;
     p.pool_cap = steal_pool_factor() * pl.grid;
     p.tail_slot0 = nslots_static;  // pool slots follow the static ones
+    if (S_grp == N && bwd_interleave()) {
+      // interleaved chunks over the whole range: at most kStealMaxC per owner
+      p.interleave = 1;
+      const int64_t need = (N + static_cast<int64_t>(pl.grid) * al::kStealMaxC - 1) /
+                           (static_cast<int64_t>(pl.grid) * al::kStealMaxC);
+      int c = p.chunk_rows;
+      if (need > c) c = static_cast<int>((need + 1) / 2 * 2);
+      p.chunk_rows = c;
+    }
   }
   // Interleaved static partition (single group): the static instance walks stages k, k+G, ...
   // -- a fixed, deterministic assignment whose CTAs sweep HBM together (AL_BWD_INTERLEAVE=0
   // restores the contiguous split)
-  if (!use_steal && !pipe_auto && n_dyn == 0 && pl.path == 1 && vec && tu.variant != 2 &&
-      tu.variant != 3 && S_grp == N && bwd_interleave())
-    p.interleave = 1;
+  if (!use_steal && n_dyn == 0 && pl.path == 1 && vec && tu.variant != 2 && S_grp == N &&
+      bwd_interleave() && (!pipe_auto || bwd_interleave() == 2))
+    p.interleave = 1;  // (also honoured by the skewed-pipeline kernel's static instance)
   if (n_dyn) {
     int dev;
     const bool full = pl.threads - 32 == p.nvec / pl.V && p.nvec % pl.V == 0;

@@ -2180,8 +2180,39 @@ __global__ void __launch_bounds__(384, 1) adaln_bwd_pipe(const BwdParams p) {
     }
   };
 
+  if (!DYN && p.interleave) {
+    // interleaved static partition (single group): stages k, k+G, ... as the producer walks
+    // them (StageWalker::init_interleaved); one (1 + scale), one slot
+    load_scale(0);
+    const int64_t step_rows = static_cast<int64_t>(p.G) * R;
+    int64_t rb = k * R;
+    CT mc[R], rc[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      mc[rr] = rb + rr < p.N ? mean_p[rb + rr] : CT(0);
+      rc[rr] = rb + rr < p.N ? rstd_p[rb + rr] : CT(0);
+    }
+    for (; rb < p.N; rb += step_rows) {
+      const int rows = p.N - rb < R ? static_cast<int>(p.N - rb) : R;
+      const int64_t nb = rb + step_rows;
+      CT mn[R], rn[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        mn[rr] = nb + rr < p.N ? mean_p[nb + rr] : CT(0);
+        rn[rr] = nb + rr < p.N ? rstd_p[nb + rr] : CT(0);
+      }
+      mbar_wait(&full[s], ph);
+      step(rb, rows, mc, rc);
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        mc[rr] = mn[rr];
+        rc[rr] = rn[rr];
+      }
+    }
+    flush(k);  // zeros when this CTA had no stage: its slot still takes part
+  }
   // static head: the producer's StageWalker sequence, segment by segment
-  int64_t row = r0;
+  int64_t row = (!DYN && p.interleave) ? r1 : r0;
   while (row < r1) {
     const int64_t g = row / p.S_grp;
     const int64_t seg_end = min((g + 1) * p.S_grp, r1);

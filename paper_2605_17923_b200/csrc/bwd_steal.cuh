@@ -37,8 +37,8 @@
 namespace al {
 
 constexpr int kStealSlots = 32;   // concurrently usable protocol states (streams / captures)
-constexpr int kStealMaxG = 640;   // CTAs per launch (<= 4 per SM)
-constexpr int kStealMaxC = 32;    // stealable chunks per owner
+constexpr int kStealMaxG = 296;   // CTAs per launch (<= 2 per SM)
+constexpr int kStealMaxC = 64;    // stealable chunks per owner
 
 struct StealSlot {
   unsigned long long word[kStealMaxG];
@@ -52,15 +52,26 @@ struct StealSlot {
 __device__ StealSlot g_steal[kStealSlots];
 
 struct ChunkGeo {
-  int64_t cstart;  // first chunked row (the chunks are the last nch * C rows of the range)
+  int64_t cstart;  // first chunked row (contiguous layout: the last nch * C rows of the range)
   int64_t group;   // group of the range's last segment
   int nch;
+  bool il;         // interleaved layout: chunk j of owner k is global chunk j * G + k
 };
 
-// Chunk geometry of owner k: identical in the owner and in every thief.
-__device__ __forceinline__ ChunkGeo chunk_geo(int64_t k, int64_t N, int64_t G, int64_t S_grp, int C) {
+// Chunk geometry of owner k: identical in the owner and in every thief.  Interleaved (single
+// group): the whole row range is cut into C-row chunks dealt round robin, chunk j of owner k =
+// global chunk j*G + k, so the owners sweep HBM together (the dynamic tail's access order) and
+// stolen chunks are the sweep's last ones.  Contiguous: the last segment of the owner's static
+// range, cut into its last nch chunks.
+__device__ __forceinline__ ChunkGeo chunk_geo(int64_t k, int64_t N, int64_t G, int64_t S_grp, int C,
+                                              bool il = false) {
+  if (il) {
+    const int64_t nc = (N + C - 1) / C;
+    ChunkGeo c{0, 0, nc > k ? static_cast<int>((nc - 1 - k) / G + 1) : 0, true};
+    return c;
+  }
   const int64_t r0 = part_begin(k, N, G), r1 = part_begin(k + 1, N, G);
-  ChunkGeo c{r1, 0, 0};
+  ChunkGeo c{r1, 0, 0, false};
   if (r1 <= r0) return c;
   c.group = (r1 - 1) / S_grp;
   const int64_t seg0 = max(r0, c.group * S_grp);
@@ -69,6 +80,9 @@ __device__ __forceinline__ ChunkGeo chunk_geo(int64_t k, int64_t N, int64_t G, i
   c.nch = static_cast<int>(n);
   c.cstart = r1 - n * C;
   return c;
+}
+__device__ __forceinline__ int64_t chunk_row0(const ChunkGeo& c, int64_t k, int64_t G, int C, int j) {
+  return c.il ? (static_cast<int64_t>(j) * G + k) * C : c.cstart + static_cast<int64_t>(j) * C;
 }
 
 __device__ __forceinline__ unsigned long long steal_word(unsigned int e, unsigned int h, unsigned int t) {
@@ -161,7 +175,7 @@ __global__ void __launch_bounds__(MAXT, 1) adaln_bwd_steal(const BwdParams p) {
     //    base + l), refilled 32 rows at a time and prefetched a block ahead;
     //  * the owner claims its next chunk with one atomicAdd on the head, issued a chunk
     //    ahead of use (it cannot fail, so it needs no CAS loop); only thieves use CAS.
-    const ChunkGeo mine = chunk_geo(k, p.N, G, p.S_grp, C);
+    const ChunkGeo mine = chunk_geo(k, p.N, G, p.S_grp, C, p.interleave != 0);
     if (lane == 0) atomicExch(&st->word[k], steal_word(E, 0u, static_cast<unsigned int>(mine.nch)));
     const uint64_t pol = policy_evict_first();
     const uint8_t* xb = static_cast<const uint8_t*>(p.x);
@@ -244,20 +258,25 @@ __global__ void __launch_bounds__(MAXT, 1) adaln_bwd_steal(const BwdParams p) {
     // the round-1 dynamic loop verbatim (no per-stage event decoding on the hot path).
     auto data = [&](int64_t row, int rows) { emit(row, rows, 0, 0, 0); };
     auto ctrl = [&](int ev, int64_t a, int64_t b) { emit(0, 0, ev, a, b); };
-    // one chunk's stages [row0, row0 + C), optionally preceded by a scale load
+    // one chunk's stages [row0, min(row0 + C, N)), optionally preceded by a scale load
     auto emit_chunk = [&](int64_t row0, bool scale, int64_t g, int last_ev) {
       if (scale) ctrl(kEvScale, g, 0);
-      for (int64_t row = row0; row < row0 + C; row += R)
-        data(row, row0 + C - row < R ? static_cast<int>(row0 + C - row) : R);
+      const int64_t end = row0 + C < p.N ? row0 + C : p.N;
+      for (int64_t row = row0; row < end; row += R)
+        data(row, end - row < R ? static_cast<int>(end - row) : R);
       if (last_ev) ctrl(last_ev, 0, 0);
     };
 
     // ---- 1. the static part: earlier segments and the pre part of the last segment ----
-    const int64_t r0 = part_begin(k, p.N, G);
+    const int64_t r0 = mine.il ? 0 : part_begin(k, p.N, G);
     int64_t scaled = -1;
+    if (mine.il && mine.nch == 0) {  // no chunk for this CTA: its slot still takes part (zeros)
+      ctrl(kEvScale, 0, 0);
+      ctrl(kEvFlush, 0, 0);
+    }
     {
       StageWalker w;
-      w.init(r0, mine.cstart, p.S_grp);
+      w.init(r0, mine.il ? 0 : mine.cstart, p.S_grp);
       int64_t prev_g = -1;
       while (!w.done()) {
         int64_t start, g;
@@ -287,7 +306,7 @@ __global__ void __launch_bounds__(MAXT, 1) adaln_bwd_steal(const BwdParams p) {
         if (lane == 0) claim = atomicAdd(&st->word[k], 1ull << 16);  // the next one, ahead
         const bool first = scaled != mine.group;
         scaled = mine.group;
-        emit_chunk(mine.cstart + static_cast<int64_t>(h) * C, first, mine.group, kEvFlushTotal);
+        emit_chunk(chunk_row0(mine, k, G, C, h), first, mine.group, kEvFlushTotal);
       }
       // the chunks thieves took, [own_head, nch), are added in order by the consumers
       ctrl(kEvMerge, 0, (mine.group << 32) | (static_cast<int64_t>(own_head) << 16) | mine.nch);
@@ -344,8 +363,8 @@ __global__ void __launch_bounds__(MAXT, 1) adaln_bwd_steal(const BwdParams p) {
       got = __shfl_sync(0xffffffffu, got, 0);
       if (got == 0xffffffffu) continue;  // lost the race: scan again
       if (lane == 0) atomicAdd(&st->stolen, 1u);
-      const ChunkGeo vg = chunk_geo(best_v, p.N, G, p.S_grp, C);
-      emit_chunk(vg.cstart + static_cast<int64_t>(got) * C, true, vg.group, 0);
+      const ChunkGeo vg = chunk_geo(best_v, p.N, G, p.S_grp, C, p.interleave != 0);
+      emit_chunk(chunk_row0(vg, best_v, G, C, got), true, vg.group, 0);
       ctrl(kEvPublish, 0,
            (static_cast<int64_t>(best_v) << 48) | (static_cast<int64_t>(got) << 32) | pool_p);
       scaled = vg.group;
