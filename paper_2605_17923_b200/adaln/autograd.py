@@ -35,16 +35,6 @@ def adaln_modulate(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor,
     return FusedAdaLNModulate.apply(x, scale, shift, eps)
 
 
-def _vector_ok(*ts) -> bool:
-    """16-byte rows and pointers: what the vector kernels take."""
-    for t in ts:
-        if t is None:
-            continue
-        if (t.shape[-1] * t.element_size()) % 16 or t.data_ptr() % 16 or not t.is_contiguous():
-            return False
-    return True
-
-
 class FusedGateResidualAdaLN(torch.autograd.Function):
     """(x_out, y) = (x + gate * f, AdaLN(x + gate * f)) as one node (al_adaln_gate_residual_forward).
 
@@ -65,15 +55,9 @@ class FusedGateResidualAdaLN(torch.autograd.Function):
         x_out, f, gate, scale, mean, rstd = ctx.saved_tensors
         # autograd materialises an unused output's gradient as zeros, so both are tensors here
         dxn, dsc, dsh = fused_backward(g_y, x_out, scale, mean, rstd)
-        if _vector_ok(dxn, g_xo, f, gate) and dxn.shape[-1] * dxn.element_size() <= 2048 * 16:
-            # one pass: G = dxn + g_xo, df = gate * G, dgate = sum_s f * G
-            G, df, dgate = fused_gate_residual_backward(dxn, g_xo, f, gate)
-        else:  # rows not 16-byte aligned: the same arithmetic as torch ops on the device
-            G = dxn + g_xo.to(dxn.dtype)
-            gb = gate.unsqueeze(-2) if gate.dim() == 2 and x_out.dim() == 3 else gate
-            df = G * gb.to(G.dtype)
-            red = tuple(range(x_out.dim() - 1)) if gate.dim() == 1 else (1,)
-            dgate = (f.float() * G.float()).sum(dim=red)
+        # one pass: G = dxn + g_xo, df = gate * G, dgate = sum_s f * G (the vector kernel for
+        # 16-byte rows, the generic kernel -- same arithmetic -- for any other width/alignment)
+        G, df, dgate = fused_gate_residual_backward(dxn, g_xo.to(dxn.dtype), f, gate)
         return (G, df, dgate.to(ctx.mod_dtypes[0]), dsc.to(ctx.mod_dtypes[1]),
                 dsh.to(ctx.mod_dtypes[2]), None)
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <atomic>
 #include <cstdarg>
 #include <cstdlib>
@@ -1659,15 +1660,46 @@ int al_qk_rmsnorm_backward(const void* qkv, int64_t row_stride, const void* wq, 
 }
 
 
+// Generic gated-residual backward plan (any width / alignment): 256 threads, [D] shared partials.
+constexpr int64_t kGrGenericCols = 8192;  // columns per CTA of the generic kernel (<= 64 KB)
+int gr_generic_plan(int64_t N, int64_t D, int dtype, Plan* out) {
+  const int cs = ct_size(dtype);
+  int dev, sms;
+  int rc = current_device(&dev);
+  if (!rc) rc = dev_sms(dev, &sms);
+  if (rc) return rc;
+  Plan pl;
+  pl.path = 0;
+  pl.threads = 256;
+  pl.smem = static_cast<size_t>(std::min<int64_t>(D, kGrGenericCols)) * cs;
+  pl.fn = with_table(dtype, [&](const auto& t) -> const void* {
+    using TT = std::remove_cv_t<std::remove_reference_t<decltype(t)>>;
+    (void)t;
+    if constexpr (std::is_same_v<TT, Table<__nv_bfloat16>>) return (const void*)al::gate_residual_bwd_generic<__nv_bfloat16>;
+    else if constexpr (std::is_same_v<TT, Table<__half>>) return (const void*)al::gate_residual_bwd_generic<__half>;
+    else if constexpr (std::is_same_v<TT, Table<double>>) return (const void*)al::gate_residual_bwd_generic<double>;
+    else return (const void*)al::gate_residual_bwd_generic<float>;
+  });
+  rc = ensure_attr(pl.fn, dev);
+  if (rc) return rc;
+  pl.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(sms) * 4, N)));
+  *out = pl;
+  return AL_OK;
+}
+
 int64_t al_gate_residual_backward_workspace_bytes(int64_t batch, int64_t seq, int64_t dim,
                                                   int64_t mod_stride, int dtype) {
   if (check_common(batch, seq, dim, mod_stride, dtype)) return -1;
   const int64_t N = batch * seq;
   if (N == 0) return 0;
-  Plan pl;
-  if (gr_plan(N, dim, dtype, &pl)) return -1;
+  // the larger of the vector and generic plans: the pointers' alignment is not known here
+  Plan pv, pg;
+  int64_t grid = 0;
+  if (gr_plan(N, dim, dtype, &pv) == AL_OK) grid = pv.grid;
+  if (gr_generic_plan(N, dim, dtype, &pg) == AL_OK) grid = std::max<int64_t>(grid, pg.grid);
+  if (grid == 0) return -1;
   const int64_t ngroups = mod_stride ? batch : 1;
-  return (pl.grid + ngroups - 1) * dim * ct_size(dtype);
+  return (grid + ngroups - 1) * dim * ct_size(dtype);
 }
 
 int al_gate_residual_backward(const void* dxn, const void* gxo, const void* f, const void* gate,
@@ -1689,12 +1721,50 @@ int al_gate_residual_backward(const void* dxn, const void* gxo, const void* f, c
   }
   if (!dxn || !f || !gate || !dx || !df || !dgate) return fail(AL_ERR_SHAPE, "null tensor pointer");
   const void* vp[6] = {dxn, gxo ? gxo : dxn, f, gate, dx, df};
-  for (const void* q : vp)
-    if (!aligned16(q)) return fail(AL_ERR_SHAPE, "gated-residual tensors must be 16-byte aligned");
-  if ((mod_stride * es) % 16 != 0) return fail(AL_ERR_SHAPE, "mod_stride must be 16-byte aligned");
+  bool vec_ok = (mod_stride * es) % 16 == 0;
+  for (const void* q : vp) vec_ok = vec_ok && aligned16(q);
   Plan pl;
-  rc = gr_plan(N, dim, dtype, &pl);
-  if (rc) return rc;
+  const bool vplan = gr_plan(N, dim, dtype, &pl) == AL_OK;
+  if (!vec_ok || !vplan) {
+    // any width or alignment: the generic kernel (same arithmetic, and the vector plan's row
+    // partition when there is one, so the results are bit-identical), scalar stage 2
+    const int vgrid = vplan ? pl.grid : 0;
+    rc = gr_generic_plan(N, dim, dtype, &pl);
+    if (rc) return rc;
+    if (vgrid) pl.grid = vgrid;
+    const int64_t nslots = pl.grid + ngroups - 1;
+    if (!workspace || workspace_bytes < nslots * dim * cs)
+      return fail(AL_ERR_WORKSPACE, "workspace too small: need %lld bytes",
+                  (long long)(nslots * dim * cs));
+    al::GRParams p = {};
+    p.dxn = dxn;
+    p.gxo = gxo;
+    p.f = f;
+    p.gate = gate;
+    p.dx = dx;
+    p.df = df;
+    p.ws = workspace;
+    p.N = N;
+    p.S_grp = mod_stride ? seq : N;
+    p.D = dim;
+    p.mod_stride = mod_stride;
+    p.nslots = nslots;
+    p.G = pl.grid;
+    const int64_t cb = std::min<int64_t>(dim, kGrGenericCols);
+    p.nvec = static_cast<int>(cb);  // the generic kernel's column-block width
+    void* args[] = {&p};
+    cudaError_t e = launch_k(pl.fn, dim3(pl.grid, static_cast<unsigned>((dim + cb - 1) / cb)),
+                             dim3(pl.threads), args, pl.smem, st, kPdlBwd1);
+    if (e != cudaSuccess) return cuda_fail(e, "gated-residual backward (generic) launch");
+    const void* rk = reduce_kernel(dtype, false);
+    void* none = nullptr;
+    int64_t G64 = pl.grid, D64 = dim, N64 = N, S64 = p.S_grp, ns = nslots;
+    void* rargs[] = {&workspace, &dgate, &none, &N64, &S64, &D64, &G64, &ns};
+    e = launch_k(rk, dim3(static_cast<unsigned>((dim + 31) / 32), static_cast<unsigned>(ngroups)),
+                 dim3(1024), rargs, 0, st, kPdlBwd2);
+    if (e != cudaSuccess) return cuda_fail(e, "gated-residual backward stage-2 launch");
+    return AL_OK;
+  }
   const int64_t nslots = pl.grid + ngroups - 1;
   const int64_t need = nslots * dim * cs;
   if (!workspace || workspace_bytes < need)

@@ -2436,7 +2436,7 @@ __global__ void __launch_bounds__(1024) adaln_bwd_reduce(const CT* __restrict__ 
   part[0][w][lane] = a;
   part[1][w][lane] = b;
   __syncthreads();
-  if (w < 2 && col < D) {
+  if (w < (two ? 2 : 1) && col < D) {
     double t = 0.0;
 #pragma unroll 8
     for (int q = 0; q < 32; ++q) t += part[w][q][lane];

@@ -386,4 +386,51 @@ __global__ void __launch_bounds__(512) gate_residual_bwd(const GRParams p) {
   }
 }
 
+// Any width / alignment (the vector kernel needs 16-byte rows and pointers): the same
+// arithmetic per element -- G = dxn + g_xo in the compute type, rounded to T; df = gate * G;
+// dgate partial += f * G (fma), rows in order -- with thread t owning columns t, t + blockDim,
+// ... and the partials in shared memory ([D] compute type), flushed per (CTA, sample) slot for
+// the scalar stage-2 kernel.  Bit-identical to the vector kernel on shapes both take.
+template <typename T>
+__global__ void __launch_bounds__(256) gate_residual_bwd_generic(const GRParams p) {
+  pdl_enter();
+  using CT = typename Traits<T>::CT;
+  extern __shared__ __align__(16) uint8_t smem[];
+  CT* acc = reinterpret_cast<CT*>(smem);
+  // blockIdx.y: a block of p.nvec columns (wide rows are split so the partials fit in shared
+  // memory); threads own columns c0 + tid, c0 + tid + blockDim, ...
+  const int64_t c0 = static_cast<int64_t>(blockIdx.y) * p.nvec;
+  const int64_t c1 = c0 + p.nvec < p.D ? c0 + p.nvec : p.D;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = part_begin(k, p.N, p.G), r1 = part_begin(k + 1, p.N, p.G);
+  const T* dxn = static_cast<const T*>(p.dxn);
+  const T* gxo = static_cast<const T*>(p.gxo);
+  const T* f = static_cast<const T*>(p.f);
+  T* dx = static_cast<T*>(p.dx);
+  T* df = static_cast<T*>(p.df);
+  CT* ws = static_cast<CT*>(p.ws);
+  int64_t row0 = r0;
+  while (row0 < r1) {
+    const int64_t g = row0 / p.S_grp;
+    const int64_t seg_end = min(r1, (g + 1) * p.S_grp);
+    const T* gate = static_cast<const T*>(p.gate) + g * p.mod_stride;
+    for (int64_t d = c0 + tid; d < c1; d += nt) acc[d - c0] = CT(0);
+    for (int64_t row = row0; row < seg_end; ++row) {
+      const int64_t o = row * p.D;
+      for (int64_t d = c0 + tid; d < c1; d += nt) {
+        CT G = to_ct(dxn[o + d]);
+        if (gxo) G = G + to_ct(gxo[o + d]);
+        const T Gt = from_ct<T>(G);
+        const CT Gr = to_ct(Gt);
+        dx[o + d] = Gt;
+        df[o + d] = from_ct<T>(to_ct(gate[d]) * Gr);
+        acc[d - c0] = fma(to_ct(f[o + d]), Gr, acc[d - c0]);
+      }
+    }
+    for (int64_t d = c0 + tid; d < c1; d += nt) ws[(k + g) * p.D + d] = acc[d - c0];
+    row0 = seg_end;
+  }
+}
+
 }  // namespace al

@@ -243,3 +243,41 @@ def test_residual_backward_kernel_vs_float64(dtype, shape, per_sample, cuda):
     assert torch.equal(dx2, dxn)
     assert max_rel_err(f64(dgate2), f64((f.double() * dxn.double()).sum(dim=1 if per_sample else (0, 1)))) <= (
         1e-11 if dtype == torch.float64 else 1e-5)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16, torch.float64])
+@pytest.mark.parametrize("shape,per_sample", [((2, 97, 1000), True), ((1, 64, 13), False),
+                                              ((3, 50, 3), True), ((2, 40, 40000), True)])
+def test_residual_backward_generic_kernel(dtype, shape, per_sample, cuda):
+    """Widths that are not 16-byte rows (and wider than the vector kernel) take the generic
+    kernel: same arithmetic, checked against the float64 restatement; no torch fallback."""
+    b, s, d = shape
+    _, f, gate, _, _ = make(b, s, d, dtype, cuda, seed=s + d, per_sample=per_sample)
+    g = torch.Generator(device="cpu").manual_seed(7)
+    dxn = torch.randn(b, s, d, generator=g).to(dtype).to(cuda)
+    gxo = torch.randn(b, s, d, generator=g).to(dtype).to(cuda)
+    dx, df, dgate = fused_gate_residual_backward(dxn, gxo, f, gate)
+    G = (dxn.double() + gxo.double()).to(dtype).double()
+    gb = gate.double()[:, None, :] if per_sample else gate.double()
+    tol = TOL[dtype]
+    assert max_rel_err(f64(dx), f64(G)) <= tol
+    assert max_rel_err(f64(df), f64(G * gb)) <= tol
+    ref = (f.double() * G).sum(dim=1 if per_sample else (0, 1))
+    assert max_rel_err(f64(dgate), f64(ref)) <= (1e-11 if dtype == torch.float64 else 1e-5)
+
+
+def test_residual_backward_generic_equals_vector_kernel(cuda):
+    """A misaligned view forces the generic kernel on a shape the vector kernel also takes: the
+    outputs are bit-identical."""
+    b, s, d = 2, 300, 1536
+    _, f, gate, _, _ = make(b, s, d, torch.bfloat16, cuda, seed=11)
+    g = torch.Generator(device="cpu").manual_seed(12)
+    dxn = torch.randn(b, s, d, generator=g).to(torch.bfloat16).to(cuda)
+    gxo = torch.randn(b, s, d, generator=g).to(torch.bfloat16).to(cuda)
+    ref = fused_gate_residual_backward(dxn, gxo, f, gate)
+    buf = torch.empty(b * s * d + 1, dtype=torch.bfloat16, device=cuda)
+    mis = buf[1:].view(b, s, d)  # 2-byte offset: not 16-byte aligned
+    mis.copy_(dxn)
+    out = fused_gate_residual_backward(mis, gxo, f, gate)
+    for a, r in zip(out, ref):
+        assert torch.equal(a, r)
