@@ -169,12 +169,10 @@ __global__ void __launch_bounds__(MAXT, 1) adaln_bwd_steal(const BwdParams p) {
   __syncthreads();
 
   if (warp == ncw) {  // ---------------- producer warp ----------------
-    // Everything here runs on all 32 lanes in step (lane 0 alone touches the ring and the
-    // claim words), so nothing on the per-stage path waits for a global round trip:
-    //  * row statistics come from a register cache (lane l holds the mean/rstd of row
-    //    base + l), refilled 32 rows at a time and prefetched a block ahead;
-    //  * the owner claims its next chunk with one atomicAdd on the head, issued a chunk
-    //    ahead of use (it cannot fail, so it needs no CAS loop); only thieves use CAS.
+    // All 32 lanes follow the control flow (the claim results are broadcast by shuffles and
+    // the victim scan is warp-wide); lane 0 alone touches the ring, the statistics and the
+    // claim words.  The owner claims its next chunk with one atomicAdd on the head, issued a
+    // chunk ahead of use (it cannot fail, so it needs no CAS loop); only thieves use CAS.
     const ChunkGeo mine = chunk_geo(k, p.N, G, p.S_grp, C, p.interleave != 0);
     if (lane == 0) atomicExch(&st->word[k], steal_word(E, 0u, static_cast<unsigned int>(mine.nch)));
     const uint64_t pol = policy_evict_first();
@@ -185,48 +183,17 @@ __global__ void __launch_bounds__(MAXT, 1) adaln_bwd_steal(const BwdParams p) {
     int s = 0;
     uint32_t f = 0;
 
-    // ---- statistics cache ----
-    int64_t cb0 = INT64_MIN / 2, cb1 = INT64_MIN / 2;
-    CT cm0 = CT(0), cr0 = CT(0), cm1 = CT(0), cr1 = CT(0);
-    auto fill = [&](int64_t base, CT& m, CT& r) {
-      const int64_t row = base + lane;
-      m = row < p.N ? mean_p[row] : CT(0);
-      r = row < p.N ? rstd_p[row] : CT(0);
-    };
-    auto stats = [&](int64_t row, int rows, CT* m, CT* r) {
-      if (!(row >= cb0 && row + rows <= cb0 + 32)) {
-        if (row >= cb1 && row + rows <= cb1 + 32) {
-          const int64_t tb = cb0;
-          cb0 = cb1;
-          cb1 = tb;
-          const CT t1 = cm0, t2 = cr0;
-          cm0 = cm1;
-          cr0 = cr1;
-          cm1 = t1;
-          cr1 = t2;
-        } else {
-          cb0 = row;
-          fill(cb0, cm0, cr0);
-        }
-      }
-      if (row - cb0 >= 8 && cb1 != cb0 + 32) {  // sequential run: prefetch the next block
-        cb1 = cb0 + 32;
-        fill(cb1, cm1, cr1);
-      }
-#pragma unroll
-      for (int rr = 0; rr < R; ++rr) {
-        const int src = static_cast<int>(row + rr - cb0) & 31;
-        const CT mv = __shfl_sync(0xffffffffu, cm0, src);
-        const CT rv = __shfl_sync(0xffffffffu, cr0, src);
-        m[rr] = rr < rows ? mv : CT(0);
-        r[rr] = rr < rows ? rv : CT(0);
-      }
-    };
-
     auto emit = [&](int64_t row, int rows, int ev, int64_t a, int64_t b) {
       CT m[R], r[R];
-      if (rows > 0) stats(row, rows, m, r);
       if (lane == 0) {
+        // the row statistics are loaded by lane 0 alone, issued before it waits for the ring
+        // slot (the wait hides their round trip); no warp-wide step on the per-stage path
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const bool ok = rr < rows;
+          m[rr] = ok ? mean_p[row + rr] : CT(0);
+          r[rr] = ok ? rstd_p[row + rr] : CT(0);
+        }
         if (f > 0) mbar_wait(&empty[s], (f - 1) & 1);
         h_row[s] = row;
         h_a[s] = a;
@@ -248,7 +215,6 @@ __global__ void __launch_bounds__(MAXT, 1) adaln_bwd_steal(const BwdParams p) {
           mbar_arrive(&full[s]);  // control-only slot: completes the phase without data
         }
       }
-      __syncwarp();
       if (++s == NS) {
         s = 0;
         ++f;
