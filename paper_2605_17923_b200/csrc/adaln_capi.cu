@@ -865,7 +865,9 @@ int steal_pool_factor() {
 int64_t pipe_max_rows() {
   static const int64_t m = [] {
     const char* v = std::getenv("AL_BWD_PIPE_ROWS");
-    return v ? static_cast<int64_t>(std::atoll(v)) : int64_t(16384);
+    // below the dynamic tail's 64-rows-per-CTA floor (9 472 rows at 148 CTAs) plus margin:
+    // at S = 14 040 the lock-step kernel's dynamic tail is faster (75.0 vs 76.3 us)
+    return v ? static_cast<int64_t>(std::atoll(v)) : int64_t(12288);
   }();
   return m;
 }
@@ -1355,7 +1357,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   // Dynamic tail (see adaln_bwd_tma): TMA path, vector stage 2, no explicit n_tile, not the
   // cooperative fused stage 2, caller did not ask for AL_BWD_DETERMINISTIC, and at least two
   // stages per CTA in the tail (which stays inside the last group).
-  // Short launches (<= pipe_max_rows() rows, ~100 rows per CTA at D = 5 120) take the
+  // Short launches (<= pipe_max_rows() rows, ~80 rows per CTA at D = 5 120) take the
   // skewed-pipeline kernel with its static partition: its barrier-free stages fill the few
   // stages a CTA has faster (B200, device timestamps: S = 1 560 / 3 600 / 7 800 and B = 4, 8
   // x 1 560: 7-9 % less time than the lock-step kernel; equal at 14 040; 3 % more at 32 760,

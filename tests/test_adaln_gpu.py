@@ -342,8 +342,8 @@ def test_dynamic_tail_backward(shape, mod, cuda):
             torch.float64: nat.AL_F64}[dt]
     plan = nat.describe_launch(1, b, s_, d, 0 if len(shape) == 2 else d, code)
     s_last = b * s_ if len(shape) == 2 else s_
-    # short 16-bit launches (<= 16 384 rows) take the skewed-pipeline kernel, statically
-    pipe = (dt in (torch.bfloat16, torch.float16) and b * s_ <= 16384
+    # short 16-bit launches (<= 12 288 rows) take the skewed-pipeline kernel, statically
+    pipe = (dt in (torch.bfloat16, torch.float16) and b * s_ <= 12288
             and plan["vecs_per_thread"] == 2)
     dynamic = (plan["path"] == "tma" and plan["rows_per_stage"] in (2, 4)
                and s_last >= 64 * plan["grid"] and not pipe)
