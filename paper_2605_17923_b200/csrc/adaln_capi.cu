@@ -402,6 +402,10 @@ const void* generic_kernel(int kernel, int dtype) {
     return kernel ? (const void*)t.bwd_generic : (const void*)t.fwd_generic;
   });
 }
+const void* reduce_grp_kernel(int dtype) {
+  return dtype == AL_F64 ? (const void*)al::adaln_bwd_reduce_grp<double>
+                         : (const void*)al::adaln_bwd_reduce_grp<float>;
+}
 const void* reduce_kernel(int dtype, bool vec) {
   if (dtype == AL_F64)
     return vec ? (const void*)al::adaln_bwd_reduce_vec<double> : (const void*)al::adaln_bwd_reduce<double>;
@@ -420,7 +424,12 @@ int ensure_attr(const void* fn, int dev) {
   if (dev < 0 || dev >= 64) return fail(AL_ERR_CUDA, "device ordinal %d out of range", dev);
   std::lock_guard<std::mutex> lk(g_attr.mu);
   if (g_attr.done[dev].count(fn)) return AL_OK;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin);
+  // the opt-in limit covers static + dynamic shared memory
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSmemOptin - static_cast<int>(fa.sharedSizeBytes));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   g_attr.done[dev].insert(fn);
   return AL_OK;
@@ -608,10 +617,13 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
         pl = Plan();
       } else {
         int64_t grid = static_cast<int64_t>(sms) * occ;
-        if (pl.path == 2) {
+        if (pl.path == 2 && pl.R != 2) {
           const int64_t rows_per_cta = static_cast<int64_t>(pl.threads / 32) * (pl.R == 4 ? 2 : 1);
           grid = std::min<int64_t>(grid, (N + rows_per_cta - 1) / rows_per_cta);
         }
+        // rows16: keep the full sms x occupancy grid for short launches too, so every SM gets
+        // the same number of rows (S = 1 560 as 195 full CTAs put 16 rows on 47 SMs and 8 on the
+        // rest: CTA end times 6.5 .. 10.3 us)
         pl.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, grid)));
       }
     }
@@ -689,6 +701,19 @@ cudaError_t launch_k(const void* fn, dim3 grid, dim3 block, void** args, size_t 
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
+// Stage 2 over many groups with few slots each (no dynamic tail): the thread-per-output kernel
+// (adaln_bwd_reduce_grp) instead of a block per (column block, group).  Launches it and returns
+// true when it applies.
+constexpr int64_t kRedGrpMinGroups = 16;
+bool launch_reduce_grp(int dtype, bool vec, int64_t ngroups, int64_t tail0, int64_t dim,
+                       void** rargs, cudaStream_t st, cudaError_t* err) {
+  if (!vec || tail0 >= 0 || ngroups < kRedGrpMinGroups) return false;
+  const int64_t items = ngroups * (dim * ct_size(dtype) / 16);
+  *err = launch_k(reduce_grp_kernel(dtype), dim3(static_cast<unsigned>((items + 255) / 256)),
+                  dim3(256), rargs, 0, st, kPdlBwd2);
+  return true;
+}
+
 al::FwdParams fwd_params(const void* x, const void* scale, const void* shift, void* y,
                          void* mean, void* rstd, int64_t seq, int64_t N, int64_t dim,
                          int64_t mod_stride, int dtype, double eps, int* nonfinite,
@@ -716,6 +741,7 @@ al::FwdParams fwd_params(const void* x, const void* scale, const void* shift, vo
   p.sched = nullptr;
   p.N_static = N;
   p.ts = nullptr;
+  p.dyn_groups = 0;
   return p;
 }
 
@@ -905,13 +931,30 @@ double bwd_dyn_frac() {
   return f;
 }
 
-void enable_dynamic_tail(const Plan& pl, al::FwdParams& p, cudaStream_t st) {
+// multi_group: the tail may span modulation groups (the plain forward; the gated-residual twin
+// stages its gate and keeps the tail in the last group).  AL_FWD_DYN_GROUPS=0 disables.
+// AL_FWD_DYN_GROUPS=2: the chunked tail for single-group launches too (A/B runs).
+int fwd_dyn_groups() {
+  static const int m = [] {
+    const char* v = std::getenv("AL_FWD_DYN_GROUPS");
+    return v ? std::atoi(v) : 1;
+  }();
+  return m;
+}
+void enable_dynamic_tail(const Plan& pl, al::FwdParams& p, cudaStream_t st, bool multi_group) {
   const double f = fwd_dyn_frac();
   if (!(f > 0.0) || pl.path != 2 || pl.R != 2) return;
   const int64_t warps = static_cast<int64_t>(pl.grid) * (pl.threads / 32);
-  // the tail stays inside the last modulation group (the kernel stages that group once)
-  const int64_t n_dyn = std::min<int64_t>(
-      static_cast<int64_t>(static_cast<double>(p.N) * (f < 1.0 ? f : 1.0)), p.S_grp);
+  const int64_t want = static_cast<int64_t>(static_cast<double>(p.N) * (f < 1.0 ? f : 1.0));
+  // Single group, or the residual twin: the tail stays inside the last modulation group (the
+  // kernel stages that group once).  Multi-sample launches (the sampler's buckets, e.g. 307 x
+  // 1 560 rows) otherwise ran a static split over 99.7 % of their rows: per-CTA end times
+  // 1 225 .. 1 665 us at that bucket (profiles/r2_multigroup.jsonl).
+  // The multi-group tail is whole groups handed out in chunks (the kernel restages per chunk).
+  const bool span = multi_group && fwd_dyn_groups() && (p.S_grp < p.N || fwd_dyn_groups() == 2);
+  const int64_t n_dyn = span ? p.N - (p.N - want) / p.S_grp * p.S_grp
+                             : std::min<int64_t>(want, p.S_grp);
+  p.dyn_groups = span ? 1 : 0;
   // short launches (< 2 tail rows per warp) are one wave anyway: the ticket round trip only
   // adds latency there (cfg3 S = 3 600: 3 739 vs 3 924 GB/s fwd+bwd)
   if (n_dyn < 2 * warps) return;
@@ -1222,7 +1265,7 @@ int al_adaln_forward(const void* x, const void* scale, const void* shift, void* 
   al::FwdParams p = fwd_params(x, scale, shift, y, mean, rstd, seq, N, dim, mod_stride, dtype,
                                eps, nonfinite, pl);
   p.ts = next_ts();
-  enable_dynamic_tail(pl, p, static_cast<cudaStream_t>(stream));
+  enable_dynamic_tail(pl, p, static_cast<cudaStream_t>(stream), true);
   return launch(pl, p, stream, "forward launch");
 }
 
@@ -1273,7 +1316,7 @@ int al_adaln_gate_residual_forward(const void* x, const void* f, const void* gat
       p.f = f;
       p.gate = gate;
       p.x_out = x_out;
-      enable_dynamic_tail(pr, p, static_cast<cudaStream_t>(stream));
+      enable_dynamic_tail(pr, p, static_cast<cudaStream_t>(stream), false);
       return launch(pr, p, stream, "gate-residual forward launch");
     }
   }
@@ -1545,9 +1588,11 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   void* rargs[] = {&workspace, &dscale, &dshift,     &p.N,      &p.S_grp, &p.D,
                    &G64,       &p.nslots, &p.N_static, &k3_tail0, &p.ts};
   const int64_t cols_per_cta = vec ? al::kRedCV * (16 / cs) : 32;
-  dim3 rgrid(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
-             static_cast<unsigned>(ngroups));
-  e = launch_k(rk, rgrid, dim3(vec ? 512 : 1024), rargs, 0, st, kPdlBwd2);
+  if (!launch_reduce_grp(dtype, vec, ngroups, k3_tail0, dim, rargs, st, &e)) {
+    dim3 rgrid(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
+               static_cast<unsigned>(ngroups));
+    e = launch_k(rk, rgrid, dim3(vec ? 512 : 1024), rargs, 0, st, kPdlBwd2);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "backward stage-2 launch");
   return AL_OK;
 }
@@ -1796,9 +1841,10 @@ int al_gate_residual_backward(const void* dxn, const void* gxo, const void* f, c
   unsigned long long* no_ts = nullptr;
   void* rargs[] = {&workspace, &dgate, &none, &N64, &S64, &D64, &G64, &ns, &N64, &tail0, &no_ts};
   const int64_t cols_per_cta = al::kRedCV * (16 / cs);
-  e = launch_k(rk, dim3(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
-                        static_cast<unsigned>(ngroups)),
-               dim3(512), rargs, 0, st, kPdlBwd2);
+  if (!launch_reduce_grp(dtype, true, ngroups, tail0, dim, rargs, st, &e))
+    e = launch_k(rk, dim3(static_cast<unsigned>((dim + cols_per_cta - 1) / cols_per_cta),
+                          static_cast<unsigned>(ngroups)),
+                 dim3(512), rargs, 0, st, kPdlBwd2);
   if (e != cudaSuccess) return cuda_fail(e, "gated-residual backward stage-2 launch");
   return AL_OK;
 }

@@ -61,6 +61,9 @@ struct FwdParams {
   unsigned int* sched;
   int64_t N_static;
   unsigned long long* ts;  // nullable: per-launch device timestamps (ptx.cuh ts_begin/ts_end)
+  // 1: the dynamic tail spans several modulation groups (multi-sample launches); rows of a group
+  // other than the CTA's staged one read (1 + scale, shift) straight from global memory
+  int dyn_groups;
 };
 
 // Ticket-counter slots for dynamically scheduled launches: one per (device, stream) for eager
@@ -765,7 +768,38 @@ __global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
     row0 = seg_end;
   }
 
-  if (p.sched != nullptr) {
+  if (p.sched != nullptr && p.dyn_groups) {
+    // Multi-group dynamic tail (multi-sample launches): whole groups [N_static / S_grp, ...)
+    // cut into chunks of 2 rows per warp that never cross a group; the CTA draws one chunk per
+    // ticket (thread 0, one chunk ahead, double-buffered in shared memory), restages the
+    // modulation when the chunk's group changes, and its warps split the chunk's rows.  One
+    // barrier per chunk; every row runs the same code as in the static part.  (Per-warp tickets
+    // with the modulation read from global memory instead measured 16-20 % slower.)
+    __shared__ long long s_tk[2];
+    const int CH = 2 * nwarp;
+    const int64_t g0 = p.N_static / p.S_grp;
+    const int64_t cpg = (p.S_grp + CH - 1) / CH;
+    const int64_t nch = ((p.N + p.S_grp - 1) / p.S_grp - g0) * cpg;
+    if (tid == 0) s_tk[0] = static_cast<long long>(atomicAdd(p.sched, 1u));
+    __syncthreads();
+    int buf = 0;
+    while (true) {
+      const int64_t t = s_tk[buf];
+      if (t >= nch) break;
+      if (tid == 0) s_tk[buf ^ 1] = static_cast<long long>(atomicAdd(p.sched, 1u));
+      const int64_t g = g0 + t / cpg;
+      const int64_t rs0 = g * p.S_grp + (t % cpg) * CH;
+      const int64_t re = min(min(rs0 + CH, (g + 1) * p.S_grp), p.N);
+      if (g != staged) {  // CTA-uniform; the previous chunk ended with a barrier
+        stage_group(g);
+        __syncthreads();
+        staged = g;
+      }
+      for (int64_t row = rs0 + warp; row < re; row += nwarp) do_row(row);
+      __syncthreads();  // the staging and the ticket buffer may be reused
+      buf ^= 1;
+    }
+  } else if (p.sched != nullptr) {
     // Dynamic tail: bandwidth is not shared evenly between SMs once the kernel is
     // memory-bound (per-CTA end times of a fully static split spread 87..122 us at cfg2), so
     // the last rows go to whichever warps are free.  The host keeps the tail inside the last
@@ -787,6 +821,8 @@ __global__ void __launch_bounds__(256, 2) adaln_fwd_rows16(const FwdParams p) {
       do_row(row);
       row = p.N_static + __shfl_sync(0xffffffffu, tn, 0);
     }
+  }
+  if (p.sched != nullptr) {
     // the last CTA out re-arms the counter pair for the next launch that draws this slot
     __syncthreads();
     if (tid == 0) {
@@ -2405,6 +2441,81 @@ __global__ void __launch_bounds__(512, 2) adaln_bwd_reduce_vec(const CT* __restr
   if (ts != nullptr) {
     __syncthreads();
     if (t == 0) ts_end(ts);
+  }
+}
+
+// Many-group form (multi-sample launches without a dynamic tail, e.g. the sampler's buckets of
+// 307 x 1 560 rows): a group's rows lie in one or two CTA ranges, so each group has only a few
+// slots and the block-per-(column block, group) grid above is thousands of CTAs of almost no work
+// -- 20 x 307 = 6 140 CTAs, ~380 us of latency-bound waves at that bucket.  Here one thread
+// owns one 16-byte column vector of one group and adds that group's slots in ascending order
+// (fp64, four slots' loads in flight), so the grid is the output size / 256 and one wave deep.
+template <typename CT>
+__global__ void __launch_bounds__(256) adaln_bwd_reduce_grp(const CT* __restrict__ ws,
+                                                          CT* __restrict__ dscale,
+                                                          CT* __restrict__ dshift, int64_t N,
+                                                          int64_t S_grp, int64_t D, int64_t G,
+                                                          int64_t nslots, int64_t Ns,
+                                                          int64_t tail0,
+                                                          unsigned long long* ts) {
+  pdl_wait();
+  constexpr int VE = 16 / sizeof(CT);
+  const int64_t nv = D / VE;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t ngroups = (N + S_grp - 1) / S_grp;
+  const bool two = dshift != nullptr;
+  if (item < ngroups * nv) {
+    const int64_t g = item / nv, col = (item % nv) * VE;
+    const int64_t first_row = g * S_grp;
+    const int64_t end_row = (g + 1) * S_grp < N ? (g + 1) * S_grp : N;
+    const int64_t last_static = (end_row < Ns ? end_row : Ns) - 1;
+    int64_t kf = 0, n1 = 0;
+    if (first_row <= last_static) {
+      kf = part_owner(first_row, Ns, G);
+      n1 = part_owner(last_static, Ns, G) - kf + 1;
+    }
+    const int64_t n2 = (tail0 >= 0 && end_row == N) ? G : 0;
+    const int64_t n = n1 + n2;
+    const CT* sc = ws + (kf + g) * D + col;
+    const CT* sh = two ? ws + (nslots + kf + g) * D + col : sc;
+    const int64_t jump = tail0 - (kf + g) - n1;
+    auto off = [&](int64_t i) { return (i < n1 ? i : i + jump) * D; };
+    double a[VE], b[VE];
+#pragma unroll
+    for (int e = 0; e < VE; ++e) a[e] = b[e] = 0.0;
+    for (int64_t i = 0; i < n; i += 4) {
+      uint4 va[4], vb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool ok = i + u < n;
+        va[u] = ok ? __ldcg(reinterpret_cast<const uint4*>(sc + off(i + u))) : make_uint4(0, 0, 0, 0);
+        vb[u] = ok && two ? __ldcg(reinterpret_cast<const uint4*>(sh + off(i + u)))
+                          : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i + u < n) {
+          const CT* pa = reinterpret_cast<const CT*>(&va[u]);
+          const CT* pb = reinterpret_cast<const CT*>(&vb[u]);
+#pragma unroll
+          for (int e = 0; e < VE; ++e) {
+            a[e] += static_cast<double>(pa[e]);
+            b[e] += static_cast<double>(pb[e]);
+          }
+        }
+      }
+    }
+    // element stores: the outputs carry no alignment requirement beyond their type's
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      dscale[g * D + col + e] = static_cast<CT>(a[e]);
+      if (two) dshift[g * D + col + e] = static_cast<CT>(b[e]);
+    }
+  }
+  pdl_launch();
+  if (ts != nullptr) {
+    __syncthreads();
+    if (threadIdx.x == 0) ts_end(ts);
   }
 }
 
