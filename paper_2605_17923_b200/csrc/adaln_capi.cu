@@ -859,13 +859,18 @@ al::StealSlot* steal_slot(int dev, cudaStream_t st) {
   return b + slot;
 }
 
-// Backward load balancing: 1 (default) = deterministic work stealing (adaln_bwd_steal) for every
-// TMA-path launch it fits; 0 = the round-1 scheme (dynamic tail unless AL_BWD_DETERMINISTIC,
-// static otherwise).  AL_BWD_STEAL overrides for A/B runs.
+// Backward load balancing.  2 (default, "auto") = deterministic work stealing (adaln_bwd_steal)
+// for multi-sample launches of short samples (>= 2 groups of <= kStealAutoMaxS rows: the
+// sampler's buckets, where the alternative is a static contiguous partition -- B200, separate
+// processes, profiles/r2_steal_buckets_ab.jsonl: 307 x 1 560 2 410 -> 2 271 us, 133 x 3 600
+// 2 400 -> 2 256, 49 x 7 800 1 917 -> 1 803, 15 x 14 040 1 080 -> 1 011; at 7 x 20 280 and
+// 2 x 32 760 the last group's dynamic tail is faster), elsewhere the dynamic tail / static
+// partition; 1 = stealing wherever it fits; 0 = never.  AL_BWD_STEAL overrides.
+constexpr int64_t kStealAutoMaxS = 16384;
 int bwd_steal_mode() {
   static const int m = [] {
     const char* v = std::getenv("AL_BWD_STEAL");
-    return v ? std::atoi(v) : 0;
+    return v ? std::atoi(v) : 2;
   }();
   return m;
 }
@@ -875,8 +880,8 @@ int bwd_steal_mode() {
 int steal_chunk_rows() {
   static const int c = [] {
     const char* v = std::getenv("AL_STEAL_CHUNK");
-    const int x = v ? std::atoi(v) : 8;
-    return x >= 2 ? (x + 1) / 2 * 2 : 8;
+    const int x = v ? std::atoi(v) : 32;  // 8 / 16 / 64 measured 1-4 % slower on the buckets
+    return x >= 2 ? (x + 1) / 2 * 2 : 32;
   }();
   return c;
 }
@@ -1433,7 +1438,9 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   const void* sfn = nullptr;
   size_t steal_smem = 0;
   // (tuning variant 4 = the round-1 scheme, for A/B runs)
-  if (bwd_steal_mode() == 1 && !pipe_auto && pl.path == 1 && vec && n_tile == 0 &&
+  const bool steal_wanted = bwd_steal_mode() == 1 ||
+                            (bwd_steal_mode() == 2 && ngroups >= 2 && S_grp <= kStealAutoMaxS);
+  if (steal_wanted && !pipe_auto && pl.path == 1 && vec && n_tile == 0 &&
       tu.variant != 2 && tu.variant != 3 && tu.variant != 4 && pl.R == 2 && pl.grid <= al::kStealMaxG &&
       N >= 2 * steal_chunk_rows() * static_cast<int64_t>(pl.grid)) {
     const int nvec_ = static_cast<int>(dim * elem_size(dtype) / 16);

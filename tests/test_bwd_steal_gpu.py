@@ -1,6 +1,10 @@
 """Deterministic work-stealing backward (bwd_steal.cuh): bit-identical dscale/dshift/dx run to
 run whatever the stealing pattern, parity with the oracle, agreement with the static partition
-(round-1 scheme, tuning variant 4) to fp32 summation order, across group layouts."""
+(round-1 scheme, tuning variant 4) to fp32 summation order, across group layouts.
+
+Multi-sample launches of short samples (>= 2 groups of <= 16 384 rows, longer than the
+short-launch limit) take the stealing kernel by default (AL_BWD_STEAL unset = auto): those cases
+run in every GPU pass.  AL_BWD_STEAL=1 forces it everywhere it fits (the remaining cases)."""
 
 import os
 
@@ -35,9 +39,37 @@ SHAPES = [(1, 32760, 5120, True), (1, 12345, 5120, True), (3, 7001, 5120, True),
           (4, 3000, 1536, True), (2, 9000, 5120, False), (1, 20000, 2048, True)]
 
 
+# the sampler's buckets at reduced size: auto-selected stealing (no environment needed)
+AUTO_SHAPES = [(3, 7001, 5120, True), (24, 1560, 5120, True), (9, 2500, 2048, True),
+               (16, 1001, 1536, True)]
+AUTO = os.environ.get("AL_BWD_STEAL") in (None, "2")
+
+
+@pytest.mark.skipif(not AUTO, reason="auto stealing disabled by AL_BWD_STEAL")
+@pytest.mark.parametrize("b,s,d,per_sample", AUTO_SHAPES)
+def test_auto_steal_buckets(b, s, d, per_sample, cuda):
+    _check_steal(b, s, d, per_sample, cuda)
+    # and against the static partition (round-1 scheme) to fp32 summation order
+    x, dy, sc = _data(b, s, d, torch.bfloat16, cuda, seed=s, per_sample=per_sample)
+    y, mu, rs = fused_forward(x, sc, sc)
+    a = fused_backward(dy, x, sc, mu, rs)
+    nat.set_tuning(1, 0, 0, 0, False, 4)
+    try:
+        ref = fused_backward(dy, x, sc, mu, rs, deterministic=True)
+    finally:
+        nat.set_tuning(1, 0, 0, 0, False, 0)
+    assert torch.equal(a[0], ref[0])
+    assert max_rel_err(f64(a[1]), f64(ref[1])) <= 2e-6
+    assert max_rel_err(f64(a[2]), f64(ref[2])) <= 2e-6
+
+
 @steal_only
 @pytest.mark.parametrize("b,s,d,per_sample", SHAPES)
 def test_steal_bitwise_reproducible_and_vs_oracle(b, s, d, per_sample, cuda):
+    _check_steal(b, s, d, per_sample, cuda)
+
+
+def _check_steal(b, s, d, per_sample, cuda):
     x, dy, sc = _data(b, s, d, torch.bfloat16, cuda, seed=s, per_sample=per_sample)
     y, mu, rs = fused_forward(x, sc, sc)
     first = fused_backward(dy, x, sc, mu, rs, deterministic=True)
@@ -147,3 +179,24 @@ def test_short_launch_pipeline_kernel(b, s, d, cuda):
     assert max_rel_err(f64(a[0]), f64(ref[0])) <= 8e-3
     assert max_rel_err(f64(a[1]), f64(ref[1])) <= 2e-6
     assert max_rel_err(f64(a[2]), f64(ref[2])) <= 2e-6
+
+
+@pytest.mark.skipif(not AUTO, reason="auto stealing disabled by AL_BWD_STEAL")
+def test_auto_steal_in_cuda_graph(cuda):
+    """Captured multi-sample launches: each capture owns its protocol slot; replays agree."""
+    x, dy, sc = _data(24, 1560, 5120, torch.bfloat16, cuda, seed=4)
+    y, mu, rs = fused_forward(x, sc, sc)
+    ref = fused_backward(dy, x, sc, mu, rs)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream(device=cuda)
+    cap.wait_stream(torch.cuda.current_stream(cuda))
+    with torch.cuda.stream(cap):
+        with torch.cuda.graph(g, stream=cap):
+            out = fused_backward(dy, x, sc, mu, rs)
+    for _ in range(4):
+        g.replay()
+        ref2 = fused_backward(dy, x, sc, mu, rs)  # eager launches between replays
+        torch.cuda.synchronize()
+        for a_, b_, c_ in zip(out, ref, ref2):
+            assert torch.equal(a_, b_) and torch.equal(c_, b_)

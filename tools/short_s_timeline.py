@@ -123,6 +123,12 @@ def main():
     if args and args[0] == "--one":  # --one B S det(0/1)
         print(json.dumps(run(int(args[2]), K=10, det=bool(int(args[3])), B=int(args[1]))), flush=True)
         return
+    if args and args[0] == "--bucket1":  # --bucket1 S det(0/1): one bucket, this process
+        from paper_2605_17923_b200.scheduler import DualConstraint, dual_constraint_batch
+        S = int(args[1])
+        B = dual_constraint_batch(S, DualConstraint(480_000.0, 3e9, 2.0))[0]
+        print(json.dumps(run(S, K=10, det=bool(int(args[2])), B=B)), flush=True)
+        return
     if args and args[0] == "--buckets":
         # cfg3 as the sampler issues it: B = the reference's dual-constraint batch for each S
         # (DualConstraint(M_mem = 480 000 tokens, M_comp = 3e9, p = 2), cluster_sim.py:332-336)
