@@ -864,8 +864,9 @@ al::StealSlot* steal_slot(int dev, cudaStream_t st) {
 // sampler's buckets, where the alternative is a static contiguous partition -- B200, separate
 // processes, profiles/r2_steal_buckets_ab.jsonl: 307 x 1 560 2 410 -> 2 271 us, 133 x 3 600
 // 2 400 -> 2 256, 49 x 7 800 1 917 -> 1 803, 15 x 14 040 1 080 -> 1 011; at 7 x 20 280 and
-// 2 x 32 760 the last group's dynamic tail is faster), elsewhere the dynamic tail / static
-// partition; 1 = stealing wherever it fits; 0 = never.  AL_BWD_STEAL overrides.
+// 2 x 32 760 the last group's dynamic tail is faster, so longer samples steal only in
+// deterministic launches), elsewhere the dynamic tail / static partition; 1 = stealing wherever
+// it fits; 0 = never.  AL_BWD_STEAL overrides.
 constexpr int64_t kStealAutoMaxS = 16384;
 int bwd_steal_mode() {
   static const int m = [] {
@@ -891,6 +892,14 @@ int steal_pool_factor() {
     return v ? std::atoi(v) : 2;
   }();
   return f;
+}
+
+int bwd_det_lean() {
+  static const int m = [] {
+    const char* v = std::getenv("AL_BWD_DET_LEAN");
+    return v ? std::atoi(v) : 1;
+  }();
+  return m;
 }
 
 int64_t pipe_max_rows() {
@@ -1438,8 +1447,12 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   const void* sfn = nullptr;
   size_t steal_smem = 0;
   // (tuning variant 4 = the round-1 scheme, for A/B runs)
-  const bool steal_wanted = bwd_steal_mode() == 1 ||
-                            (bwd_steal_mode() == 2 && ngroups >= 2 && S_grp <= kStealAutoMaxS);
+  // (deterministic multi-group launches of longer samples have no dynamic tail to lose: 7 x
+  // 20 280 730 -> 707 us, 2 x 32 760 341 -> 343)
+  const bool steal_wanted =
+      bwd_steal_mode() == 1 ||
+      (bwd_steal_mode() == 2 && ngroups >= 2 &&
+       (S_grp <= kStealAutoMaxS || (flags & AL_BWD_DETERMINISTIC)));
   if (steal_wanted && !pipe_auto && pl.path == 1 && vec && n_tile == 0 &&
       tu.variant != 2 && tu.variant != 3 && tu.variant != 4 && pl.R == 2 && pl.grid <= al::kStealMaxG &&
       N >= 2 * steal_chunk_rows() * static_cast<int64_t>(pl.grid)) {
@@ -1528,6 +1541,16 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   if (!use_steal && n_dyn == 0 && pl.path == 1 && vec && tu.variant != 2 && S_grp == N &&
       bwd_interleave() && (!pipe_auto || bwd_interleave() == 2))
     p.interleave = 1;  // (also honoured by the skewed-pipeline kernel's static instance)
+  // Deterministic single-group launches: the interleaved static walk on the dynamic instance's
+  // lean stage body (bit-identical to the static instance; B200, profiles/r2_det_lean.jsonl:
+  // cfg2 169.2 -> 164.1 us, S = 75 600 371.8 -> 360.6, 14 040 80.9 -> 78.9; the dynamic tail
+  // 161.1 / 357.3 / 76.5 on the same box).  AL_BWD_DET_LEAN=0 restores the static instance.
+  if (p.interleave && !pipe_auto && n_dyn == 0 && bwd_det_lean()) {
+    int dev;
+    const bool full = pl.threads - 32 == p.nvec / pl.V && p.nvec % pl.V == 0;
+    const void* dfn = tma_dyn_kernel(dtype, pl.V, pl.R, full);
+    if (dfn && cudaGetDevice(&dev) == cudaSuccess && ensure_attr(dfn, dev) == AL_OK) pl.fn = dfn;
+  }
   if (n_dyn) {
     int dev;
     const bool full = pl.threads - 32 == p.nvec / pl.V && p.nvec % pl.V == 0;

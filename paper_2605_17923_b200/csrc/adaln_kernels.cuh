@@ -1429,7 +1429,7 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       const uint8_t* xb = static_cast<const uint8_t*>(p.x);
       const uint8_t* db = static_cast<const uint8_t*>(p.dy);
       StageWalker w;
-      if (!DYN && p.interleave) w.init_interleaved(k, p.G, p.N, R);
+      if (p.interleave) w.init_interleaved(k, p.G, p.N, R);
       else w.init(r0, r1, p.S_grp);
       int s = 0;
       uint32_t f = 0;
@@ -1653,11 +1653,42 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
     ++it;
   };
 
+  if (p.interleave) {
+    // Interleaved static walk of a single group (deterministic launches, no ticket): stages k,
+    // k + G, k + 2G, ... through the same lean stage body; partials to slot k.
+    load_scale(0);
+    const int64_t nst = (p.N + R - 1) / R;
+    CT mc[R], rc[R];
+    auto fetch = [&](int64_t st, CT* m, CT* r) {
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        const bool ok = st < nst && st * R + rr < p.N;
+        m[rr] = ok ? mean_p[st * R + rr] : CT(0);
+        r[rr] = ok ? rstd_p[st * R + rr] : CT(0);
+      }
+    };
+    fetch(k, mc, rc);
+    for (int64_t st = k; st < nst; st += p.G) {
+      CT mn[R], rn[R];
+      fetch(st + p.G, mn, rn);
+      mbar_wait(&full[s], ph);
+      const int64_t rb = st * R;
+      const int rows = p.N - rb < R ? static_cast<int>(p.N - rb) : R;
+      if (rows == R) stage(std::true_type{}, rb, R, mc, rc);
+      else stage(std::false_type{}, rb, rows, mc, rc);
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        mc[rr] = mn[rr];
+        rc[rr] = rn[rr];
+      }
+    }
+    flush(k);
+  }
   // Static head.  Segments = the CTA's rows of one reduction group (sample): (1+scale) loaded
   // once, then full R-row stages, one predicated tail stage, and the group's partials flushed
   // to slot k + g.  Statistics are prefetched one stage ahead.  The producer's StageWalker
   // issues the same sequence.
-  int64_t row = r0;
+  int64_t row = p.interleave ? r1 : r0;
   while (row < r1) {
     const int64_t g = row / p.S_grp;
     const int64_t seg_end = min((g + 1) * p.S_grp, r1);
@@ -1962,7 +1993,7 @@ __global__ void __launch_bounds__(384, 1) adaln_bwd_pipe(const BwdParams p) {
       const uint8_t* xb = static_cast<const uint8_t*>(p.x);
       const uint8_t* db = static_cast<const uint8_t*>(p.dy);
       StageWalker w;
-      if (!DYN && p.interleave) w.init_interleaved(k, p.G, p.N, R);
+      if (p.interleave) w.init_interleaved(k, p.G, p.N, R);
       else w.init(r0, r1, p.S_grp);
       int s = 0;
       uint32_t f = 0;
