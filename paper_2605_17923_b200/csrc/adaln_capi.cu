@@ -704,10 +704,18 @@ cudaError_t launch_k(const void* fn, dim3 grid, dim3 block, void** args, size_t 
 // Stage 2 over many groups with few slots each (no dynamic tail): the thread-per-output kernel
 // (adaln_bwd_reduce_grp) instead of a block per (column block, group).  Launches it and returns
 // true when it applies.
-constexpr int64_t kRedGrpMinGroups = 16;
+// From 8 groups (B200, profiles/r2_reduce_grp_threshold.jsonl: 15 x 14 040 1 011 -> 996 us;
+// 2 and 4 groups lose 7-20 us with it, 7 x 20 280 is neutral).  AL_RED_GRP_MIN overrides.
+int64_t red_grp_min_groups() {
+  static const int64_t m = [] {
+    const char* v = std::getenv("AL_RED_GRP_MIN");
+    return v ? std::atoll(v) : 8;
+  }();
+  return m;
+}
 bool launch_reduce_grp(int dtype, bool vec, int64_t ngroups, int64_t tail0, int64_t dim,
                        void** rargs, cudaStream_t st, cudaError_t* err) {
-  if (!vec || tail0 >= 0 || ngroups < kRedGrpMinGroups) return false;
+  if (!vec || tail0 >= 0 || ngroups < red_grp_min_groups()) return false;
   const int64_t items = ngroups * (dim * ct_size(dtype) / 16);
   *err = launch_k(reduce_grp_kernel(dtype), dim3(static_cast<unsigned>((items + 255) / 256)),
                   dim3(256), rargs, 0, st, kPdlBwd2);

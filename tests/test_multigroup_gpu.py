@@ -3,7 +3,7 @@
 * forward: the dynamic row tail spans modulation groups (rows of a group other than the CTA's
   staged one read (1 + scale, shift) from global memory) -- every row must equal the same row
   computed by a one-sample launch, bit for bit, whichever path it took;
-* backward stage 2 over many groups (adaln_bwd_reduce_grp, >= 16 groups without a dynamic tail)
+* backward stage 2 over many groups (adaln_bwd_reduce_grp, >= 8 groups without a dynamic tail)
   -- dscale/dshift vs the oracle-style fp64 reference, and per-sample equality with one-sample
   launches where the partial layout makes the sums identical;
 * non-finite modulation rows in tail groups are still rejected.
