@@ -550,6 +550,9 @@ def main():
         # (set, not setdefault: images that export NCCL_DEBUG=WARN would silence them)
         os.environ["NCCL_DEBUG"] = "INFO"
         os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+        # to stderr: NCCL logs to stdout by default, after the JSON line (which must stay the
+        # last line of rank 0's stdout)
+        os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup(args)
     try:
