@@ -617,13 +617,14 @@ int make_plan(int kernel, int64_t N, int64_t D, int64_t mod_stride, int dtype, i
         pl = Plan();
       } else {
         int64_t grid = static_cast<int64_t>(sms) * occ;
-        if (pl.path == 2 && pl.R != 2) {
+        if (pl.path == 2) {
+          // short launches: enough CTAs for one row per warp, rounded UP to a multiple of the
+          // SM count so every SM gets the same number of rows (S = 1 560 as 195 full CTAs put 16
+          // rows on 47 SMs and 8 on the rest: CTA end times 6.5 .. 10.3 us; 296 CTAs: 9.3 us)
           const int64_t rows_per_cta = static_cast<int64_t>(pl.threads / 32) * (pl.R == 4 ? 2 : 1);
-          grid = std::min<int64_t>(grid, (N + rows_per_cta - 1) / rows_per_cta);
+          const int64_t need = (N + rows_per_cta - 1) / rows_per_cta;
+          grid = std::min<int64_t>(grid, (need + sms - 1) / sms * sms);
         }
-        // rows16: keep the full sms x occupancy grid for short launches too, so every SM gets
-        // the same number of rows (S = 1 560 as 195 full CTAs put 16 rows on 47 SMs and 8 on the
-        // rest: CTA end times 6.5 .. 10.3 us)
         pl.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, grid)));
       }
     }

@@ -16,7 +16,12 @@
 // every CTA), writes it to a pool slot and publishes it with an epoch-tagged flag.  The owner,
 // after its own chunks, adds the stolen c_j in chunk order.  The sums therefore do not depend
 // on who computed which chunk: dscale/dshift are bit-identical run to run, while the tail of
-// the kernel is balanced at chunk granularity (C = 8 rows, ~6 us of one SM's work).
+// the kernel is balanced at chunk granularity (C = 32 rows by default).
+//
+// Selected automatically (adaln_capi.cu bwd_steal_mode) for multi-sample launches: there the
+// alternative is a static contiguous partition, and stealing measured 6 % faster (307 x 1 560
+// ... 15 x 14 040 rows, profiles/r2_steal_buckets_ab.jsonl) and bit-reproducible.  Single-sample
+// launches keep the dynamic tail / interleaved static walk of adaln_bwd_tma.
 //
 // Protocol state lives in a per-stream slot of device memory (StealSlot, zero at module load):
 //  * epoch: each launch uses E = epoch + 1 (read by every CTA at entry; the previous launch on
