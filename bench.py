@@ -416,7 +416,13 @@ def run_ours(args, world, rank, local):
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, world)
     barrier(world)
     es = 2
-    h2d = (x.numel() * es + 2 * D * es) + (2 * x.numel() * es + D * es + 2 * S * 4)
+    # forward: x, scale, shift in; y, mean, rstd out.  backward: dy (+ x unless the forward's
+    # device copy of x is still valid -- the host API keeps it, _host.py), scale, mean, rstd in;
+    # dx, dscale, dshift out
+    from paper_2605_17923_b200.adaln._host import _resident
+
+    x_again = 0 if _resident.enabled else x.numel() * es
+    h2d = (x.numel() * es + 2 * D * es) + (x.numel() * es + x_again + D * es + 2 * S * 4)
     d2h = (x.numel() * es + 2 * S * 4) + (x.numel() * es + 2 * D * 4)
     e2e_gbs = world * nb["total"] / e2e_s / 1e9
 
@@ -515,7 +521,10 @@ def run_ours(args, world, rank, local):
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "step_ms_min_max": [round(1e3 * min(step_s), 2), round(1e3 * max(step_s), 2)],
                 "step_ms_median": round(1e3 * statistics.median(step_s), 2),
-                "path": "adaln_forward + adaln_backward_naive on pinned torch CPU bf16 tensors"},
+                "path": "adaln_forward + adaln_backward_naive on pinned torch CPU bf16 tensors "
+                        "(the backward reuses the forward's device copy of x)"
+                        if _resident.enabled else
+                        "adaln_forward + adaln_backward_naive on pinned torch CPU bf16 tensors"},
         "cpu_baseline": cpu,
         "gpu_launches": 3 * K,  # fwd K1 + bwd K2 + K3 per step (the deterministic leg is outside)
         "clocks": clk.summary(),

@@ -11,7 +11,9 @@ Argument kinds:
     scale/shift [B, D] (the north-star layout; dscale/dshift come back [B, D]).
   * torch CPU tensors: streamed through the GPU in row chunks with host->device copies,
     kernels and device->host copies overlapped on two streams (``_host.py``); results come
-    back in pinned host memory in the input dtype.
+    back in pinned host memory in the input dtype.  The forward keeps its device copy of x
+    for a following backward on the same (unmodified, by version counter) tensor
+    (``release_resident()`` frees it; ``AL_HOST_RESIDENT=0`` disables).
   * numpy arrays / sequences: the reference's semantics -- cast to float64 (``_as_f64``,
     adaln/__init__.py:81-85), computed in fp64 on the GPU, returned as float64 numpy arrays.
 
@@ -30,7 +32,7 @@ import numpy as np
 import torch
 
 from ..errors import InvalidTile, ShapeMismatch, StaleStats
-from ._host import host_backward, host_forward
+from ._host import host_backward, host_forward, release_resident  # noqa: F401
 from ._ops import fused_backward, fused_forward, fused_gate_residual_forward, geometry, stat_dtype  # noqa: F401
 
 __all__ = [

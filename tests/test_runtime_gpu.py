@@ -126,6 +126,41 @@ def test_host_api_results_survive_later_calls(cuda):
     assert not torch.equal(o2.y, keep)
 
 
+def test_host_backward_reuses_the_forwards_device_copy_of_x(cuda):
+    """forward(x) then backward(dy, x): the backward uses the forward's device copy of x (no
+    second upload) with results bit-identical to a backward that uploads x; an in-place change
+    of x (version counter) or another tensor object invalidates it; a collected x frees it."""
+    import gc
+
+    from paper_2605_17923_b200.adaln import adaln_backward_naive
+
+    g = np.random.default_rng(11)
+    x = torch.from_numpy(g.standard_normal((3, 700, 2048), dtype=np.float32)).to(torch.bfloat16)
+    x = x.pin_memory()
+    dy = torch.from_numpy(g.standard_normal((3, 700, 2048), dtype=np.float32)).to(torch.bfloat16)
+    sc = (0.1 * torch.randn(3, 2048)).to(torch.bfloat16)
+    out = adaln_forward(x, sc, sc, check_finite=False)
+    assert _host._resident.get(x, cuda) is not None
+    res = adaln_backward_naive(dy, x, sc, out.mu, out.rstd, check_finite=False)
+    ref = adaln_backward_naive(dy, x.clone(), sc, out.mu, out.rstd, check_finite=False)  # uploads
+    for a, b in zip((res.dx, res.dscale, res.dshift), (ref.dx, ref.dscale, ref.dshift)):
+        assert torch.equal(a, b)
+    # in-place change after the forward: the resident copy is stale and must not be used
+    x.mul_(2.0)
+    assert _host._resident.get(x, cuda) is None
+    res2 = adaln_backward_naive(dy, x, sc, out.mu, out.rstd, check_finite=False)
+    ref2 = adaln_backward_naive(dy, x.clone(), sc, out.mu, out.rstd, check_finite=False)
+    for a, b in zip((res2.dx, res2.dscale, res2.dshift), (ref2.dx, ref2.dscale, ref2.dshift)):
+        assert torch.equal(a, b)
+    assert not torch.equal(res2.dx, res.dx)
+    # a collected input releases its device copy
+    adaln_forward(x, sc, sc, check_finite=False)
+    assert _host._resident.get(x, cuda) is not None
+    del x
+    gc.collect()
+    assert cuda.index not in _host._resident._e
+
+
 def test_launch_timestamps(cuda):
     x, sc, sh, dy = _inputs(1, 32760, 5120, cuda, 7)
     ts = torch.empty(4, 2, dtype=torch.int64, device=cuda)
