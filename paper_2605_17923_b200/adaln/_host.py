@@ -32,7 +32,8 @@ import torch
 from ..errors import NonFiniteInput
 from ._ops import fused_backward, fused_forward, geometry, stat_dtype
 
-CHUNK_BYTES = 32 << 20
+# host->device bytes per pipeline chunk (AL_HOST_CHUNK_MB overrides, A/B runs)
+CHUNK_BYTES = int(float(os.environ.get("AL_HOST_CHUNK_MB", "32")) * (1 << 20))
 
 _side_streams: dict = {}
 
@@ -200,7 +201,9 @@ def host_backward(dy: torch.Tensor, x: torch.Tensor, scale: torch.Tensor, mu: to
     main, side = torch.cuda.current_stream(dev), _side(dev)
     xres = _resident.get(x, dev)  # the forward's device copy of this x, if still valid
     parts = []  # (b0, b1, dscale chunk, dshift chunk) on the device
-    for b0, b1, s0, s1 in _chunks(B, S, 2 * D * x.element_size()):
+    # chunks sized by the bytes that actually move in (dy, and x unless it is resident)
+    in_row = (1 if xres is not None else 2) * D * x.element_size()
+    for b0, b1, s0, s1 in _chunks(B, S, in_row):
         xd = xres[b0:b1, s0:s1] if xres is not None else x3[b0:b1, s0:s1].to(dev, non_blocking=True)
         dyd = dy3[b0:b1, s0:s1].to(dev, non_blocking=True)
         mud = mu2[b0:b1, s0:s1].to(dev, non_blocking=True)

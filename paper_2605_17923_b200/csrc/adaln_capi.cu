@@ -954,8 +954,10 @@ double bwd_dyn_frac() {
   return f;
 }
 
-// multi_group: the tail may span modulation groups (the plain forward; the gated-residual twin
-// stages its gate and keeps the tail in the last group).  AL_FWD_DYN_GROUPS=0 disables.
+// multi_group: the tail may span modulation groups (chunked, restaged per chunk; the plain
+// forward -- the gated-residual twin measured 2-4 % slower with it at D = 1 536, 300 x 1 600 ..
+// 8 x 9 450, profiles/r2_resid_multigroup_tail.jsonl, and keeps its tail in the last group).
+// AL_FWD_DYN_GROUPS=0 disables.
 // AL_FWD_DYN_GROUPS=2: the chunked tail for single-group launches too (A/B runs).
 int fwd_dyn_groups() {
   static const int m = [] {

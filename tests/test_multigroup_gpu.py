@@ -75,3 +75,22 @@ def test_forward_multigroup_nonfinite_tail_scale(cuda):
     sh[39, 5] = float("inf")
     with pytest.raises(NonFiniteInput):
         adaln_forward(x, sc, sh)
+
+
+@pytest.mark.parametrize("b,s,d", [(40, 250, 1536), (24, 999, 2048)])
+def test_gate_residual_multigroup_tail_bitwise_per_sample(b, s, d, cuda):
+    """The gated-residual twin's chunked multi-group tail (restages gate, 1 + scale, shift per
+    chunk): every sample equal to a one-sample launch, bit for bit."""
+    from paper_2605_17923_b200.adaln._ops import fused_gate_residual_forward
+
+    g = torch.Generator(device="cpu").manual_seed(3)
+    x = torch.randn(b, s, d, generator=g).to(torch.bfloat16).to(cuda)
+    f = torch.randn(b, s, d, generator=g).to(torch.bfloat16).to(cuda)
+    gate, sc, sh = ((0.3 * torch.randn(b, d, generator=g)).to(torch.bfloat16).to(cuda)
+                    for _ in range(3))
+    full = fused_gate_residual_forward(x, f, gate, sc, sh)
+    for i in range(b):
+        one = fused_gate_residual_forward(x[i:i + 1], f[i:i + 1], gate[i:i + 1], sc[i:i + 1],
+                                          sh[i:i + 1])
+        for a, r in zip(full, one):
+            assert torch.equal(a[i:i + 1], r), i

@@ -33,7 +33,10 @@ def timed(fn, iters=40):
 
 def main():
     dev = torch.device("cuda", 0)
-    for B, S, D in [(1, 32760, 5120), (4, 8190, 5120), (8, 9450, 1536), (2, 32760, 1536)]:
+    shapes = [(1, 32760, 5120), (4, 8190, 5120), (8, 9450, 1536), (2, 32760, 1536)]
+    if len(sys.argv) > 1:  # B,S,D ...
+        shapes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]]
+    for B, S, D in shapes:
         x = torch.randn(B, S, D, device=dev, dtype=torch.bfloat16)
         f = torch.randn_like(x)
         gate = 0.3 * torch.randn(B, D, device=dev, dtype=torch.bfloat16)

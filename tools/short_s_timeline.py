@@ -26,7 +26,7 @@ from paper_2605_17923_b200.adaln._ops import (backward_workspace_bytes, fused_ba
                                               fused_forward)
 
 L2 = 126 << 20
-D = 5120
+D = int(__import__("os").environ.get("AL_PROBE_D", "5120"))  # feature width (AL_PROBE_D)
 
 
 def cta_spread(lib, kernel, grid):
