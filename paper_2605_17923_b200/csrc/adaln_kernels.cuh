@@ -1748,6 +1748,7 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
     }
     flush(p.tail_slot0 + k);
   }
+  if (tid == 0) AL_TRACE_INFO(it);
   } else {
     // Static-only instance (deterministic launches): the predicated single-instance loop.  Its
     // CTAs stay issue-bound at one common rate; the leaner DYN loop makes them memory-bound
@@ -2719,4 +2720,5 @@ __global__ void __launch_bounds__(256) adaln_bwd_generic(const BwdParams p) {
 }  // namespace al
 
 #include "bwd_steal.cuh"
+#include "bwd8.cuh"
 

@@ -123,7 +123,17 @@ __device__ __forceinline__ void cta_trace(int kernel, int which) {
   if (blockIdx.x < 4096) g_cta_trace[kernel][2 * blockIdx.x + which] = t;
 }
 #define AL_TRACE(kernel, which) ::al::cta_trace(kernel, which)
+// (smid << 32 | stages) per CTA of the last traced backward: how the dynamic walk spread the
+// stages over SMs of unequal bandwidth
+__device__ unsigned long long g_cta_info[4096];
+__device__ __forceinline__ void cta_info(unsigned long long stages) {
+  unsigned sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  if (blockIdx.x < 4096) g_cta_info[blockIdx.x] = (static_cast<unsigned long long>(sm) << 32) | stages;
+}
+#define AL_TRACE_INFO(stages) ::al::cta_info(stages)
 #else
+#define AL_TRACE_INFO(stages) ((void)0)
 #define AL_TRACE(kernel, which) ((void)0)
 #endif
 
