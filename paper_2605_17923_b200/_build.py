@@ -25,7 +25,7 @@ ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 # parallel and linked into one library (tools/gen_instances.py writes the instance lists)
 SOURCES = ["adaln_capi.cu", "instances_f32.cu", "instances_bf16.cu", "instances_f16.cu",
            "instances_f64.cu"]
-HEADERS = ["adaln_kernels.cuh", "bwd_steal.cuh", "bwd8.cuh", "block_kernels.cuh", "dtype.cuh", "ptx.cuh",
+HEADERS = ["adaln_kernels.cuh", "bwd_steal.cuh", "block_kernels.cuh", "dtype.cuh", "ptx.cuh",
            "instances_extern.inc"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-diag-suppress", "20279,20281"]

@@ -95,7 +95,6 @@ struct Table {
   BwdFn bwd_full[3][3];  // nvec == V * consumers: ownership predicates compiled out
   BwdFn bwd_dyn[3][2];   // dynamic-tail instances, R = 2 / 4 (non-deterministic launches)
   BwdFn bwd_dyn_full[3][2];
-  BwdFn bwd8 = nullptr;  // 8-warp backward for 16-bit rows of 513..768 vectors (bwd8.cuh)
   FwdFn fwd_generic;
   BwdFn bwd_generic;
   Table() {
@@ -167,7 +166,6 @@ struct Table {
     bwd_dyn_full[2][0] = al::adaln_bwd_tma<T, 4, 2, true, true>;
     bwd_dyn[2][1] = al::adaln_bwd_tma<T, 4, 4, false, true>;
     bwd_dyn_full[2][1] = al::adaln_bwd_tma<T, 4, 4, true, true>;
-    if constexpr (sizeof(T) == 2) bwd8 = al::adaln_bwd8<T>;
     fwd_generic = al::adaln_fwd_generic<T>;
     bwd_generic = al::adaln_bwd_generic<T>;
   }
@@ -943,16 +941,6 @@ double fwd_dyn_frac() {
   return f;
 }
 
-// 8-warp backward (bwd8.cuh, K2b) for single-group 16-bit launches of 513..768 vectors per
-// row: 1 = on, 0 = the 11-warp K2.  AL_BWD8 overrides.
-int bwd8_mode() {
-  static const int m = [] {
-    const char* v = std::getenv("AL_BWD8");
-    return v ? std::atoi(v) : 0;
-  }();
-  return m;
-}
-
 // Backward: fraction of the rows in the dynamic tail (capped at the last group).  Measured at
 // cfg2 (tools/bw_probe.py, B200): backward 5 870 GB/s static (the previous loop; 5 087 for
 // this loop, whose faster CTAs expose the uneven bandwidth split), 5 999 / 6 077 / 6 107 /
@@ -1591,27 +1579,6 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
       p.sched = slot;
       p.N_static = N - n_dyn;
       p.tail_slot0 = nslots_static;
-    }
-  }
-  // K2b (bwd8.cuh): the 8-warp, producer-less ring for the two single-group walks it implements
-  // -- every stage from the ticket counter, or the deterministic interleaved walk
-  if (bwd8_mode() && !use_steal && !pipe_auto && pl.path == 1 && vec && n_tile == 0 &&
-      tu.variant == 0 && tu.V == 0 && (tu.R == 0 || tu.R == 2) && S_grp == N &&
-      (dtype == AL_BF16 || dtype == AL_F16) && p.nvec > 512 && p.nvec <= 768 &&
-      ((p.sched != nullptr && p.N_static == 0) || (p.sched == nullptr && p.interleave))) {
-    const void* fn8 = with_table(dtype, [](const auto& t) { return (const void*)t.bwd8; });
-    const size_t stage = 2 * 2 * static_cast<size_t>(p.row_bytes);
-    const size_t extra = 256 + 2 * 8 * 2 * 2 * 4 + 16;  // barriers + headers + row-sum scratch
-    int ns = 8;
-    while (ns > 3 && ns * stage + ns * 20 + extra > static_cast<size_t>(kSmemOptin)) --ns;
-    int dev;
-    if (fn8 != nullptr && ns * stage + ns * 20 + extra <= static_cast<size_t>(kSmemOptin) &&
-        cudaGetDevice(&dev) == cudaSuccess && ensure_attr(fn8, dev) == AL_OK) {
-      pl.fn = fn8;
-      pl.threads = 256;
-      pl.NS = ns;
-      pl.smem = ns * stage + ns * 20 + extra;
-      p.nstages = ns;
     }
   }
   // Skewed-pipeline stage 1 (variant 3 while under evaluation): same ring/slot contract, its

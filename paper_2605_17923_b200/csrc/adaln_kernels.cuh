@@ -2720,5 +2720,4 @@ __global__ void __launch_bounds__(256) adaln_bwd_generic(const BwdParams p) {
 }  // namespace al
 
 #include "bwd_steal.cuh"
-#include "bwd8.cuh"
 

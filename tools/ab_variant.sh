@@ -11,7 +11,7 @@ mkdir -p "$tmp/p/csrc" "$tmp/include"
 if [ -d "$src" ]; then
   cp -r "$src"/. "$tmp/p/csrc/"; cp "$root/include/adaln_b200.h" "$tmp/include/"
 else
-  for f in adaln_capi.cu adaln_kernels.cuh bwd_steal.cuh bwd8.cuh block_kernels.cuh dtype.cuh ptx.cuh instances_extern.inc; do
+  for f in adaln_capi.cu adaln_kernels.cuh bwd_steal.cuh block_kernels.cuh dtype.cuh ptx.cuh instances_extern.inc; do
     git -C "$root" show "$src:paper_2605_17923_b200/csrc/$f" > "$tmp/p/csrc/$f"; done
   git -C "$root" show "$src:include/adaln_b200.h" > "$tmp/include/adaln_b200.h"
 fi
