@@ -425,6 +425,31 @@ def run_ours(args, world, rank, local):
     h2d = (x.numel() * es + 2 * D * es) + (x.numel() * es + x_again + D * es + 2 * S * 4)
     d2h = (x.numel() * es + 2 * S * 4) + (x.numel() * es + 2 * D * 4)
     e2e_gbs = world * nb["total"] / e2e_s / 1e9
+    # the PCIe ceiling of that leg on this box: one cfg2 tensor host->device and another
+    # device->host at the same time (two streams, pinned memory, best of 3); the host API moves
+    # h2d + d2h bytes per step, so (h2d + d2h) / duplex rate bounds its step time
+    pcie = None
+    try:
+        hb = torch.empty_like(xh, pin_memory=True)
+        db = torch.empty_like(x)
+        s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        best = float("inf")
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            with torch.cuda.stream(s1):
+                db.copy_(xh, non_blocking=True)
+            with torch.cuda.stream(s2):
+                hb.copy_(y, non_blocking=True)
+            torch.cuda.synchronize(dev)
+            best = min(best, time.perf_counter() - t0)
+        duplex = 2 * xh.numel() * es / best / 1e9
+        pcie = {"duplex_gbs": round(duplex, 1),
+                "e2e_ceiling": round(world * nb["total"] / ((h2d + d2h) / (duplex * 1e9)) / 1e9, 1)
+                if duplex > 0 else None}
+        del hb, db
+    except Exception as exc:  # noqa: BLE001 - informative only
+        pcie = {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
     # measured 'N-GPU imbalance %' of the metric: the DP step on this process group under
     # each bucket plan (equal token, the reference's dual constraint, the reference fitter's
@@ -521,6 +546,7 @@ def run_ours(args, world, rank, local):
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "step_ms_min_max": [round(1e3 * min(step_s), 2), round(1e3 * max(step_s), 2)],
                 "step_ms_median": round(1e3 * statistics.median(step_s), 2),
+                "pcie": pcie,
                 "path": "adaln_forward + adaln_backward_naive on pinned torch CPU bf16 tensors "
                         "(the backward reuses the forward's device copy of x)"
                         if _resident.enabled else
