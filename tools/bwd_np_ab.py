@@ -1,11 +1,11 @@
 #!/usr/bin/env python3
-"""K2b (bwd8.cuh, 8 warps, no producer warp) vs K2 (adaln_bwd_tma, 11 warps): backward device
+"""Producer-less backward (bwd_np.cuh: 12 warps x V=2 or 8 warps x V=3) vs K2 (adaln_bwd_tma, 11 warps): backward device
 time (per-launch %globaltimer stamps, median of K eager launches after warm-up) at single-sample
 lengths, dynamic and deterministic, plus a parity check of the selected kernel against a torch
-fp64 restatement and run-to-run bit-identity of the deterministic mode.  AL_BWD8 is read once
+fp64 restatement and run-to-run bit-identity of the deterministic mode.  AL_BWD_NP is read once
 per process, so run it once per setting:
 
-    AL_BWD8=0 python tools/bwd8_ab.py; AL_BWD8=1 python tools/bwd8_ab.py
+    for m in 0 12 8; do AL_BWD_NP=$m python tools/bwd_np_ab.py; done
 """
 import json
 import os
@@ -23,7 +23,7 @@ from paper_2605_17923_b200.adaln._ops import (backward_workspace_bytes, fused_ba
 D, K = 5120, 20
 dev = torch.device("cuda", 0)
 lens = [int(a) for a in sys.argv[1:]] or [14040, 20280, 32760, 46800, 75600]
-tag = os.environ.get("AL_BWD8", "0")
+tag = os.environ.get("AL_BWD_NP", "0")
 for S in lens:
     g = torch.Generator(device=dev).manual_seed(S)
     x = torch.randn(1, S, D, device=dev, generator=g).to(torch.bfloat16)
@@ -35,7 +35,7 @@ for S in lens:
     dsc = torch.empty(1, D, device=dev)
     dsh = torch.empty(1, D, device=dev)
     ws = torch.empty(backward_workspace_bytes(x, sc), dtype=torch.uint8, device=dev)
-    out = {"S": S, "AL_BWD8": tag}
+    out = {"S": S, "AL_BWD_NP": tag}
     nbytes = 3 * S * D * 2 + 8 * S + D * 2 + 8 * D
     for det in (False, True):
         for _ in range(5):
