@@ -941,6 +941,22 @@ double fwd_dyn_frac() {
   return f;
 }
 
+// K2 / K2s ring-slot release point (DESIGN 3.2.1): each consumer warp arrives on the slot's
+// empty barrier 2 = as soon as its shared loads of the stage are issued (the arrive's release
+// semantics order them), 1 = after phase 1 (before the row-sum reduction and the stage
+// barrier), 0 = after the stage barrier (the round-2 kernels before the pace study).  Releasing
+// earlier keeps more of the ring in flight: B200 A/B (profiles/r2_bwd_early_release.jsonl),
+// cfg2 deterministic 164.0 -> 161.2 (1) -> 160.1 us (2), dynamic 166.4 -> 164.4 (1) / 164.8
+// (2); 14 040 .. 75 600 alike.  Default: 1 for ticketed launches, 2 otherwise.  AL_BWD_EARLY
+// overrides.
+int bwd_early_release(bool ticketed) {
+  static const int m = [] {
+    const char* v = std::getenv("AL_BWD_EARLY");
+    return v ? std::atoi(v) : -1;
+  }();
+  return m >= 0 ? m : (ticketed ? 1 : 2);
+}
+
 // Backward: fraction of the rows in the dynamic tail (capped at the last group).  Measured at
 // cfg2 (tools/bw_probe.py, B200): backward 5 870 GB/s static (the previous loop; 5 087 for
 // this loop, whose faster CTAs expose the uneven bandwidth split), 5 999 / 6 077 / 6 107 /
@@ -1534,6 +1550,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   p.chunk_rows = steal_chunk_rows();
   p.pool_cap = 0;
   p.interleave = 0;
+  p.early_release = 0;  // set at launch (bwd_early_release)
   if (use_steal) {
     pl.fn = sfn;
     pl.smem = steal_smem;
@@ -1613,6 +1630,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   // needs a cooperative launch (all CTAs co-resident) and a zeroed counter at the workspace
   // tail.  Otherwise stage 2 is a second kernel.
   // opt-in (variant 2): measured equal to the separate kernel on B200 (0.189 ms both)
+  p.early_release = bwd_early_release(p.sched != nullptr);
   const bool fuse = pl.path == 1 && vec && tu.variant == 2 &&
                     workspace_bytes >= need + 16 && cooperative_ok(pl);
   void* args[] = {&p};
@@ -1625,6 +1643,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
     if (e != cudaSuccess) return cuda_fail(e, "backward (fused) cooperative launch");
     return AL_OK;
   }
+  p.early_release = bwd_early_release(p.sched != nullptr);
   e = launch_k(pl.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, st, kPdlBwd1);
   if (e != cudaSuccess) return cuda_fail(e, "backward stage-1 launch");
   // stage 2: 16-byte vector form when every partial row is 16-byte aligned

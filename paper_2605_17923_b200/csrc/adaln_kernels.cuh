@@ -111,6 +111,9 @@ struct BwdParams {
   int pool_cap;
   // interleaved static partition (single group, adaln_bwd_tma static instance)
   int interleave;
+  // 1: a consumer warp releases its ring slot as soon as its phase-1 loads are consumed, not
+  // after the stage barrier (adaln_bwd_tma); more bytes stay in flight per SM
+  int early_release;
 };
 
 // Row partition shared by stage 1 and stage 2.
@@ -1565,11 +1568,25 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
     // phase 1: row sums of g and g*xhat; column accumulators of dy and dy*xhat.
     // Rows past `rows` (stage tail) and columns past D read as zero, so every lane runs the
     // same instruction stream and the shuffles below are convergent.
+    // the stage's x and dy vectors into registers first (mode 2 releases the slot right here)
+    uint4 rawx[R][V], rawd[R][V];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const bool ok = (ALL || rr < rows) && (vmask >> j & 1);
+        const uint32_t o = static_cast<uint32_t>(rr * RB + coff[j]);
+        rawx[rr][j] = ok ? ld_shared_v4_u32(stx_u + o) : make_uint4(0, 0, 0, 0);
+        rawd[rr][j] = ok ? ld_shared_v4_u32(std_u + o) : make_uint4(0, 0, 0, 0);
+      }
+    if (p.early_release == 2) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
     P xh[R][V][NP], gg[R][V][NP];
     CT rowsum[R * 2];
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      const bool live = ALL || rr < rows;
       const P nm = splat2(-mc[rr]), r2 = splat2(rc[rr]);
       // 16-bit inputs: xhat = x*r - m*r in one FFMA2 (the product is exact inside the FMA;
       // the absolute error ~|m| r 2^-24 is far below the inputs' own 2^-9 rounding)
@@ -1578,11 +1595,9 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       P sg[2] = {splat2(CT(0)), splat2(CT(0))}, sgx[2] = {splat2(CT(0)), splat2(CT(0))};
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        const bool ok = live && (vmask >> j & 1);
         P xv[NP], dv[NP];
-        const uint32_t o = static_cast<uint32_t>(rr * RB + coff[j]);
-        unpack2<T>(ok ? ld_shared_v4_u32(stx_u + o) : make_uint4(0, 0, 0, 0), xv);
-        unpack2<T>(ok ? ld_shared_v4_u32(std_u + o) : make_uint4(0, 0, 0, 0), dv);
+        unpack2<T>(rawx[rr][j], xv);
+        unpack2<T>(rawd[rr][j], dv);
 #pragma unroll
         for (int e = 0; e < NP; ++e) {
           if constexpr (sizeof(T) == 2) xh[rr][j][e] = fma2(xv[e], r2, nmr);
@@ -1598,15 +1613,24 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       rowsum[2 * rr] = tsg.x + tsg.y;
       rowsum[2 * rr + 1] = tsgx.x + tsgx.y;
     }
+    // this warp has the stage in registers (its shared loads are ordered before the arrive by
+    // the mbarrier's release semantics): release the slot now, so the producer refills it
+    // while the row sums are reduced and the barrier waits -- ~25 % of a stage sooner
+    if (p.early_release == 1) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
     {
       constexpr int NV = 2 * R, GRP = 32 / NV;
       const CT u = warp_reduce_scatter<NV>(rowsum, lane);
       if ((lane & (GRP - 1)) == 0) rd[warp * NV + lane / GRP] = u;
     }
     named_bar_sync(1, nc);
-    // every consumer has read this stage into registers: release the slot to the producer
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (!p.early_release) {
+      // every consumer has read this stage into registers: release the slot to the producer
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
 
     // cross-warp totals, spread over the lanes: rd holds ncw x NV values [warp][k]; lane l
     // sums entries l, l+32, ... (all of index k = l % NV), lanes of equal k are combined by a
@@ -1813,11 +1837,25 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
     // phase 1: row sums of g and g*xhat; column accumulators of dy and dy*xhat.
     // Rows past `rows` (stage tail) and columns past D read as zero, so every lane runs the
     // same instruction stream and the shuffles below are convergent.
+    // the stage's x and dy vectors into registers first (mode 2 releases the slot right here)
+    uint4 rawx[R][V], rawd[R][V];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const bool ok = (rr < rows) && (vmask >> j & 1);
+        const uint32_t o = static_cast<uint32_t>(rr * RB + coff[j]);
+        rawx[rr][j] = ok ? ld_shared_v4_u32(stx_u + o) : make_uint4(0, 0, 0, 0);
+        rawd[rr][j] = ok ? ld_shared_v4_u32(std_u + o) : make_uint4(0, 0, 0, 0);
+      }
+    if (p.early_release == 2) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
     P xh[R][V][NP], gg[R][V][NP];
     CT rowsum[R * 2];
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      const bool live = rr < rows;
       const P nm = splat2(-mcur[rr]), r2 = splat2(rcur[rr]);
       // 16-bit inputs: xhat = x*r - m*r in one FFMA2 (the product is exact inside the FMA;
       // the absolute error ~|m| r 2^-24 is far below the inputs' own 2^-9 rounding)
@@ -1826,11 +1864,9 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       P sg[2] = {splat2(CT(0)), splat2(CT(0))}, sgx[2] = {splat2(CT(0)), splat2(CT(0))};
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        const bool ok = live && (vmask >> j & 1);
         P xv[NP], dv[NP];
-        const uint32_t o = static_cast<uint32_t>(rr * RB + coff[j]);
-        unpack2<T>(ok ? ld_shared_v4_u32(stx_u + o) : make_uint4(0, 0, 0, 0), xv);
-        unpack2<T>(ok ? ld_shared_v4_u32(std_u + o) : make_uint4(0, 0, 0, 0), dv);
+        unpack2<T>(rawx[rr][j], xv);
+        unpack2<T>(rawd[rr][j], dv);
 #pragma unroll
         for (int e = 0; e < NP; ++e) {
           if constexpr (sizeof(T) == 2) xh[rr][j][e] = fma2(xv[e], r2, nmr);
@@ -1846,15 +1882,24 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       rowsum[2 * rr] = tsg.x + tsg.y;
       rowsum[2 * rr + 1] = tsgx.x + tsgx.y;
     }
+    // this warp has the stage in registers (its shared loads are ordered before the arrive by
+    // the mbarrier's release semantics): release the slot now, so the producer refills it
+    // while the row sums are reduced and the barrier waits -- ~25 % of a stage sooner
+    if (p.early_release == 1) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
     {
       constexpr int NV = 2 * R, GRP = 32 / NV;
       const CT u = warp_reduce_scatter<NV>(rowsum, lane);
       if ((lane & (GRP - 1)) == 0) rd[warp * NV + lane / GRP] = u;
     }
     named_bar_sync(1, nc);
-    // every consumer has read this stage into registers: release the slot to the producer
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (!p.early_release) {
+      // every consumer has read this stage into registers: release the slot to the producer
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
 
     // cross-warp totals, spread over the lanes: rd holds ncw x NV values [warp][k]; lane l
     // sums entries l, l+32, ... (all of index k = l % NV), lanes of equal k are combined by a

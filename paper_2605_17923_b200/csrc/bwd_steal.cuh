@@ -440,21 +440,33 @@ __global__ void __launch_bounds__(MAXT, 1) adaln_bwd_steal(const BwdParams p) {
     const uint32_t stx_u = smem_addr(smem) + static_cast<uint32_t>(s * stage_bytes);
     const uint32_t std_u = stx_u + static_cast<uint32_t>(R * RB);
     CT* rd = red + (it & 1) * (ncw * R * 2);
+    // the stage's x and dy vectors into registers first (mode 2 releases the slot right here)
+    uint4 rawx[R][V], rawd[R][V];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const bool ok = (ALL || rr < rows) && (vmask >> j & 1);
+        const uint32_t o = static_cast<uint32_t>(rr * RB + coff[j]);
+        rawx[rr][j] = ok ? ld_shared_v4_u32(stx_u + o) : make_uint4(0, 0, 0, 0);
+        rawd[rr][j] = ok ? ld_shared_v4_u32(std_u + o) : make_uint4(0, 0, 0, 0);
+      }
+    if (p.early_release == 2) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
     P xh[R][V][NP], gg[R][V][NP];
     CT rowsum[R * 2];
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      const bool live = ALL || rr < rows;
       const P nm = splat2(-mc[rr]), r2 = splat2(rc[rr]);
       const P nmr = splat2(-mc[rr] * rc[rr]);
       P sg[2] = {splat2(CT(0)), splat2(CT(0))}, sgx[2] = {splat2(CT(0)), splat2(CT(0))};
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        const bool ok = live && (vmask >> j & 1);
         P xv[NP], dv[NP];
-        const uint32_t o = static_cast<uint32_t>(rr * RB + coff[j]);
-        unpack2<T>(ok ? ld_shared_v4_u32(stx_u + o) : make_uint4(0, 0, 0, 0), xv);
-        unpack2<T>(ok ? ld_shared_v4_u32(std_u + o) : make_uint4(0, 0, 0, 0), dv);
+        unpack2<T>(rawx[rr][j], xv);
+        unpack2<T>(rawd[rr][j], dv);
 #pragma unroll
         for (int e = 0; e < NP; ++e) {
           if constexpr (sizeof(T) == 2) xh[rr][j][e] = fma2(xv[e], r2, nmr);
@@ -470,14 +482,20 @@ __global__ void __launch_bounds__(MAXT, 1) adaln_bwd_steal(const BwdParams p) {
       rowsum[2 * rr] = tsg.x + tsg.y;
       rowsum[2 * rr + 1] = tsgx.x + tsgx.y;
     }
+    if (p.early_release == 1) {  // as in adaln_bwd_tma: release once this warp's loads are consumed
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
     {
       constexpr int NV = 2 * R, GRP = 32 / NV;
       const CT u = warp_reduce_scatter<NV>(rowsum, lane);
       if ((lane & (GRP - 1)) == 0) rd[warp * NV + lane / GRP] = u;
     }
     named_bar_sync(1, nc);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (!p.early_release) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
     CT tot[2 * R];
     {
       constexpr int NV = 2 * R;

@@ -23,7 +23,7 @@ from paper_2605_17923_b200.adaln._ops import (backward_workspace_bytes, fused_ba
 D, K = 5120, 20
 dev = torch.device("cuda", 0)
 lens = [int(a) for a in sys.argv[1:]] or [14040, 20280, 32760, 46800, 75600]
-tag = os.environ.get("AL_BWD_NP", "0")
+tag = ",".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith("AL_BWD")) or "default"
 for S in lens:
     g = torch.Generator(device=dev).manual_seed(S)
     x = torch.randn(1, S, D, device=dev, generator=g).to(torch.bfloat16)
@@ -35,7 +35,7 @@ for S in lens:
     dsc = torch.empty(1, D, device=dev)
     dsh = torch.empty(1, D, device=dev)
     ws = torch.empty(backward_workspace_bytes(x, sc), dtype=torch.uint8, device=dev)
-    out = {"S": S, "AL_BWD_NP": tag}
+    out = {"S": S, "env": tag}
     nbytes = 3 * S * D * 2 + 8 * S + D * 2 + 8 * D
     for det in (False, True):
         for _ in range(5):
