@@ -957,6 +957,22 @@ int bwd_early_release(bool ticketed) {
   return m >= 0 ? m : (ticketed ? 1 : 2);
 }
 
+// Single-group launches (one sample, or scale/shift broadcast): 1 = the interleaved static walk
+// in either mode, 0 = a ticketed dynamic tail when the caller does not ask for determinism.
+// With the slot released as soon as a stage is in registers (bwd_early_release) the fixed
+// interleaved walk is as fast as the ticket walk or faster -- its producer computes the next
+// stage's address instead of waiting on a ticket and the statistics loads it implies -- so
+// the training path and the reference API now run the same bit-reproducible schedule.  B200
+// (profiles/r2_bwd_single_group_walk.jsonl): cfg2 160.1 vs 164.4 us, 75 600 352.9 vs 362.2 us
+// on one box, within 1 % either way on another.  AL_BWD_TICKET=1 restores the ticket walk.
+int bwd_single_group_static() {
+  static const int m = [] {
+    const char* v = std::getenv("AL_BWD_TICKET");
+    return v ? (std::atoi(v) ? 0 : 1) : 1;
+  }();
+  return m;
+}
+
 // Backward: fraction of the rows in the dynamic tail (capped at the last group).  Measured at
 // cfg2 (tools/bw_probe.py, B200): backward 5 870 GB/s static (the previous loop; 5 087 for
 // this loop, whose faster CTAs expose the uneven bandwidth split), 5 999 / 6 077 / 6 107 /
@@ -1456,7 +1472,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
                          (dtype == AL_BF16 || dtype == AL_F16);
   int64_t n_dyn = 0;
   if (!pipe_auto && pl.path == 1 && vec && n_tile == 0 && tu.variant != 2 &&
-      !(flags & AL_BWD_DETERMINISTIC)) {
+      !(flags & AL_BWD_DETERMINISTIC) && !(S_grp == N && bwd_single_group_static())) {
     const double f = bwd_dyn_frac();
     n_dyn = std::min<int64_t>(static_cast<int64_t>(static_cast<double>(N) * (f < 1.0 ? f : 1.0)),
                               S_grp);
