@@ -15,9 +15,9 @@ ROOT = Path(__file__).resolve().parent.parent
 OBJ = ROOT / "paper_2605_17923_b200" / "_lib" / "obj"
 KERNELS = {
     "adaln_fwd_rows16<bf16, 20, 0> (cfg2 forward)": ("instances_bf16.o", "_ZN2al16adaln_fwd_rows16I13__nv_bfloat16Li20ELb0EEEvNS_9FwdParamsE"),
-    "adaln_bwd_tma<bf16, 2, 2, 1, 1> (cfg2 backward, dynamic tail)": ("instances_bf16.o", "_ZN2al13adaln_bwd_tmaI13__nv_bfloat16Li2ELi2ELb1ELb1EEEvNS_9BwdParamsE"),
-    "adaln_bwd_tma<bf16, 2, 2, 1, 0> (cfg2 backward, deterministic)": ("instances_bf16.o", "_ZN2al13adaln_bwd_tmaI13__nv_bfloat16Li2ELi2ELb1ELb0EEEvNS_9BwdParamsE"),
-    "adaln_bwd_pipe<bf16, 2, 2, 1, 0> (short launches)": ("adaln_capi.o", "_ZN2al14adaln_bwd_pipeI13__nv_bfloat16Li2ELi2ELb1ELb0EEEvNS_9BwdParamsE"),
+    "adaln_bwd_tma<bf16, 2, 2, 1, 1> (cfg2 backward: lean stage body, interleaved walk by default, ticketed tail)": ("instances_bf16.o", "_ZN2al13adaln_bwd_tmaI13__nv_bfloat16Li2ELi2ELb1ELb1EEEvNS_9BwdParamsE"),
+    "adaln_bwd_tma<bf16, 2, 2, 1, 0> (static instance, kept for non-interleaved static launches)": ("instances_bf16.o", "_ZN2al13adaln_bwd_tmaI13__nv_bfloat16Li2ELi2ELb1ELb0EEEvNS_9BwdParamsE"),
+    "adaln_bwd_pipe<bf16, 2, 2, 1, 0> (short launches)": ("instances_bf16.o", "_ZN2al14adaln_bwd_pipeI13__nv_bfloat16Li2ELi2ELb1ELb0EEEvNS_9BwdParamsE"),
     "adaln_bwd_reduce_vec<float> (stage 2)": ("instances_f32.o", "_ZN2al20adaln_bwd_reduce_vecIfEEvPKT_PS1_S4_lllllllPy"),
 }
 WATCH = ["UBLKCP", "SYNCS", "FFMA2", "FADD2", "FMUL2", "FHADD", "F2FP", "LDS", "STS", "LDG", "STG",
