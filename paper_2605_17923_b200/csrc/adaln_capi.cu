@@ -716,7 +716,7 @@ int64_t red_grp_min_groups() {
 }
 bool launch_reduce_grp(int dtype, bool vec, int64_t ngroups, int64_t tail0, int64_t dim,
                        void** rargs, cudaStream_t st, cudaError_t* err) {
-  if (!vec || tail0 >= 0 || ngroups < red_grp_min_groups()) return false;
+  if (!vec || tail0 != -1 || ngroups < red_grp_min_groups()) return false;
   const int64_t items = ngroups * (dim * ct_size(dtype) / 16);
   *err = launch_k(reduce_grp_kernel(dtype), dim3(static_cast<unsigned>((items + 255) / 256)),
                   dim3(256), rargs, 0, st, kPdlBwd2);
@@ -969,6 +969,19 @@ int bwd_single_group_static() {
   static const int m = [] {
     const char* v = std::getenv("AL_BWD_TICKET");
     return v ? (std::atoi(v) ? 0 : 1) : 1;
+  }();
+  return m;
+}
+
+// Group-sequential interleaved walk for multi-sample launches of long samples (see
+// al_adaln_backward): 1 = deterministic launches and launches of <= 4 samples, 2 = all
+// launches, 0 = off.  AL_BWD_GROUP_WALK.  B200 (profiles/r2_bwd_group_walk.jsonl): 2 x 32 760
+// deterministic 347 -> 312 us, non-deterministic 325 -> 313; 7 x 20 280 deterministic
+// 702 -> 686.5 us, non-deterministic 670.4 (static + ticketed last sample) vs 688 walked.
+int bwd_group_walk() {
+  static const int m = [] {
+    const char* v = std::getenv("AL_BWD_GROUP_WALK");
+    return v ? std::atoi(v) : 1;
   }();
   return m;
 }
@@ -1418,7 +1431,10 @@ int64_t al_adaln_backward_workspace_bytes(int64_t batch, int64_t seq, int64_t di
   const int64_t ngroups = mod_stride ? batch : 1;
   // static slots (G + groups - 1) + the larger of the dynamic tail's G slots and the work
   // stealing pool (2G); + 16 bytes: the fused stage-2 grid-barrier counter
-  return 2 * (std::max(pa.grid, pg.grid) + ngroups - 1 + 2 * pa.grid) * dim * ct_size(dtype) + 16;
+  int64_t slots = std::max(pa.grid, pg.grid) + ngroups - 1 + 2 * pa.grid;
+  // the group-sequential walk of long samples: G slots per sample
+  if (ngroups >= 2 && seq > kStealAutoMaxS) slots = std::max<int64_t>(slots, pa.grid * ngroups);
+  return 2 * slots * dim * ct_size(dtype) + 16;
 }
 
 int al_adaln_backward(const void* dy, const void* x, const void* scale, const void* mean,
@@ -1490,6 +1506,24 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   // static partition wherever it fits (TMA path with 2-row stages, vector stage 2, default
   // tiling, >= 2 chunks per CTA); dscale/dshift are then bit-identical run to run whatever the
   // caller's determinism flag.
+  // Group-sequential interleaved walk (bwd_group_walk): multi-sample launches of long samples
+  // (> kStealAutoMaxS rows each; deterministic, or at most 4 samples) walk each sample like a
+  // single-sample launch, one sample after the other, with G partial slots per sample -- if the
+  // caller's workspace holds them (al_adaln_backward_workspace_bytes sizes for it).
+  bool group_walk = false;
+  if (bwd_group_walk() && !pipe_auto && pl.path == 1 && vec && n_tile == 0 && tu.variant == 0 &&
+      ngroups >= 2 && S_grp > kStealAutoMaxS &&
+      ((flags & AL_BWD_DETERMINISTIC) || bwd_group_walk() == 2 || ngroups <= 4) &&
+      workspace_bytes >= 2 * static_cast<int64_t>(pl.grid) * ngroups * dim * cs) {
+    int dev;
+    const bool full = pl.threads - 32 == dim * elem_size(dtype) / 16 / pl.V &&
+                      (dim * elem_size(dtype) / 16) % pl.V == 0;
+    const void* gfn = tma_dyn_kernel(dtype, pl.V, pl.R, full);
+    if (gfn && cudaGetDevice(&dev) == cudaSuccess && ensure_attr(gfn, dev) == AL_OK) {
+      group_walk = true;
+      n_dyn = 0;
+    }
+  }
   bool use_steal = false;
   al::StealSlot* sslot = nullptr;
   const void* sfn = nullptr;
@@ -1501,7 +1535,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
       bwd_steal_mode() == 1 ||
       (bwd_steal_mode() == 2 && ngroups >= 2 &&
        (S_grp <= kStealAutoMaxS || (flags & AL_BWD_DETERMINISTIC)));
-  if (steal_wanted && !pipe_auto && pl.path == 1 && vec && n_tile == 0 &&
+  if (!group_walk && steal_wanted && !pipe_auto && pl.path == 1 && vec && n_tile == 0 &&
       tu.variant != 2 && tu.variant != 3 && tu.variant != 4 && pl.R == 2 && pl.grid <= al::kStealMaxG &&
       N >= 2 * steal_chunk_rows() * static_cast<int64_t>(pl.grid)) {
     const int nvec_ = static_cast<int>(dim * elem_size(dtype) / 16);
@@ -1530,8 +1564,9 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
       }
     }
   }
-  const int64_t nslots = nslots_static + (use_steal ? steal_pool_factor() * pl.grid
-                                                    : (n_dyn ? pl.grid : 0));
+  const int64_t nslots = group_walk ? static_cast<int64_t>(pl.grid) * ngroups
+                                    : nslots_static + (use_steal ? steal_pool_factor() * pl.grid
+                                                                 : (n_dyn ? pl.grid : 0));
   const int64_t need = 2 * nslots * dim * cs;
   if (!workspace || workspace_bytes < need) {
     return fail(AL_ERR_WORKSPACE, "workspace too small: need %lld bytes, got %lld",
@@ -1590,6 +1625,11 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   if (!use_steal && n_dyn == 0 && pl.path == 1 && vec && tu.variant != 2 && S_grp == N &&
       bwd_interleave() && (!pipe_auto || bwd_interleave() == 2))
     p.interleave = 1;  // (also honoured by the skewed-pipeline kernel's static instance)
+  if (group_walk) {
+    const bool full = pl.threads - 32 == p.nvec / pl.V && p.nvec % pl.V == 0;
+    p.interleave = 2;
+    pl.fn = tma_dyn_kernel(dtype, pl.V, pl.R, full);
+  }
   // Deterministic single-group launches: the interleaved static walk on the dynamic instance's
   // lean stage body (bit-identical to the static instance; B200, profiles/r2_det_lean.jsonl:
   // cfg2 169.2 -> 164.1 us, S = 75 600 371.8 -> 360.6, 14 040 80.9 -> 78.9; the dynamic tail
@@ -1665,7 +1705,8 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   // stage 2: 16-byte vector form when every partial row is 16-byte aligned
   const void* rk = reduce_kernel(dtype, vec);
   int64_t G64 = pl.grid;
-  int64_t k3_tail0 = use_steal ? -1 : p.tail_slot0;  // stolen partials are merged by owners
+  // stolen partials are merged by owners; -2: the group walk's slot map (g*G .. g*G + G - 1)
+  int64_t k3_tail0 = group_walk ? -2 : (use_steal ? -1 : p.tail_slot0);
   void* rargs[] = {&workspace, &dscale, &dshift,     &p.N,      &p.S_grp, &p.D,
                    &G64,       &p.nslots, &p.N_static, &k3_tail0, &p.ts};
   const int64_t cols_per_cta = vec ? al::kRedCV * (16 / cs) : 32;

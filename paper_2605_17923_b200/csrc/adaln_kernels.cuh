@@ -1432,7 +1432,8 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       const uint8_t* xb = static_cast<const uint8_t*>(p.x);
       const uint8_t* db = static_cast<const uint8_t*>(p.dy);
       StageWalker w;
-      if (p.interleave) w.init_interleaved(k, p.G, p.N, R);
+      if (p.interleave == 2) w.init(0, 0, p.S_grp);  // empty: the group walk below
+      else if (p.interleave) w.init_interleaved(k, p.G, p.N, R);
       else w.init(r0, r1, p.S_grp);
       int s = 0;
       uint32_t f = 0;
@@ -1448,6 +1449,21 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
           ++f;
         }
       };
+      if (p.interleave == 2) {
+        // group-sequential interleaved walk (multi-sample launches of long samples): the
+        // interleaved walk of group 0, then of group 1, ... (same order as the consumers)
+        const int64_t ng = (p.N + p.S_grp - 1) / p.S_grp;
+        for (int64_t gi = 0; gi < ng; ++gi) {
+          const int64_t g0 = gi * p.S_grp, g1 = g0 + p.S_grp < p.N ? g0 + p.S_grp : p.N;
+          const int64_t nst = (g1 - g0 + R - 1) / R;
+          for (int64_t st = k; st < nst; st += p.G) {
+            const int64_t start = g0 + st * R;
+            const int rows = g1 - start < R ? static_cast<int>(g1 - start) : R;
+            if (f > 0) mbar_wait(&empty[s], (f - 1) & 1);
+            issue(start, rows);
+          }
+        }
+      }
       while (!w.done()) {
         int64_t start, g;
         const int rows = w.next(R, start, g);
@@ -1677,7 +1693,44 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
     ++it;
   };
 
-  if (p.interleave) {
+  if (p.interleave == 2) {
+    // Group-sequential interleaved walk: for each group g, stages k, k + G, ... of that group
+    // (rows g*S_grp + st*R), (1 + scale) restaged per group, partials to slot g*G + k -- every
+    // CTA flushes every group's slot (zeros if it drew no stage there); stage 2 adds slots
+    // g*G .. g*G + G - 1 in order (tail0 = -2).
+    const int64_t ng = (p.N + p.S_grp - 1) / p.S_grp;
+    for (int64_t gi = 0; gi < ng; ++gi) {
+      load_scale(gi);
+      const int64_t g0 = gi * p.S_grp, g1 = g0 + p.S_grp < p.N ? g0 + p.S_grp : p.N;
+      const int64_t nst = (g1 - g0 + R - 1) / R;
+      CT mc[R], rc[R];
+      auto fetch = [&](int64_t st, CT* m, CT* r) {
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int64_t row = g0 + st * R + rr;
+          const bool ok = st < nst && row < g1;
+          m[rr] = ok ? mean_p[row] : CT(0);
+          r[rr] = ok ? rstd_p[row] : CT(0);
+        }
+      };
+      fetch(k, mc, rc);
+      for (int64_t st = k; st < nst; st += p.G) {
+        CT mn[R], rn[R];
+        fetch(st + p.G, mn, rn);
+        mbar_wait(&full[s], ph);
+        const int64_t rb = g0 + st * R;
+        const int rows = g1 - rb < R ? static_cast<int>(g1 - rb) : R;
+        if (rows == R) stage(std::true_type{}, rb, R, mc, rc);
+        else stage(std::false_type{}, rb, rows, mc, rc);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          mc[rr] = mn[rr];
+          rc[rr] = rn[rr];
+        }
+      }
+      flush(gi * p.G + k);
+    }
+  } else if (p.interleave) {
     // Interleaved static walk of a single group (deterministic launches, no ticket): stages k,
     // k + G, k + 2G, ... through the same lean stage body; partials to slot k.
     load_scale(0);
@@ -2431,7 +2484,10 @@ __global__ void __launch_bounds__(512, 2) adaln_bwd_reduce_vec(const CT* __restr
   const int64_t end_row = (g + 1) * S_grp < N ? (g + 1) * S_grp : N;
   const int64_t last_static = (end_row < Ns ? end_row : Ns) - 1;
   int64_t kf = 0, n1 = 0;
-  if (first_row <= last_static) {
+  if (tail0 <= -2) {  // group-sequential walk: slots g*G .. g*G + G - 1
+    kf = g * G - g;
+    n1 = G;
+  } else if (first_row <= last_static) {
     kf = part_owner(first_row, Ns, G);
     n1 = part_owner(last_static, Ns, G) - kf + 1;
   }
