@@ -215,6 +215,20 @@ const void* tma_dyn_kernel(int dtype, int V, int R, bool full) {
     return full ? (const void*)t.bwd_dyn_full[a][b] : (const void*)t.bwd_dyn[a][b];
   });
 }
+// group-sequential walk instance (GW): V = 2, R = 2 plans (every D with 129..704 vectors per
+// row), or nullptr (the launch then keeps stealing / the static split)
+const void* tma_gw_kernel(int dtype, int V, int R, bool full) {
+  if (V != 2 || R != 2) return nullptr;
+  switch (dtype) {
+    case AL_BF16: return full ? (const void*)al::adaln_bwd_tma<__nv_bfloat16, 2, 2, true, true, true>
+                              : (const void*)al::adaln_bwd_tma<__nv_bfloat16, 2, 2, false, true, true>;
+    case AL_F16: return full ? (const void*)al::adaln_bwd_tma<__half, 2, 2, true, true, true>
+                             : (const void*)al::adaln_bwd_tma<__half, 2, 2, false, true, true>;
+    case AL_F32: return full ? (const void*)al::adaln_bwd_tma<float, 2, 2, true, true, true>
+                             : (const void*)al::adaln_bwd_tma<float, 2, 2, false, true, true>;
+    default: return nullptr;
+  }
+}
 // skewed-pipeline backward (adaln_bwd_pipe): bf16/fp16, V in {1, 2, 4}, R in {1, 2}
 template <typename T, int V>
 const void* pipe_t(int R, bool full, bool dyn) {
@@ -942,24 +956,24 @@ double fwd_dyn_frac() {
 }
 
 // K2 / K2s ring-slot release point (DESIGN 3.2.1): each consumer warp arrives on the slot's
-// empty barrier 2 = as soon as its shared loads of the stage are issued (the arrive's release
-// semantics order them), 1 = after phase 1 (before the row-sum reduction and the stage
-// barrier), 0 = after the stage barrier (the round-2 kernels before the pace study).  Releasing
-// earlier keeps more of the ring in flight: B200 A/B (profiles/r2_bwd_early_release.jsonl),
-// cfg2 deterministic 164.0 -> 161.2 (1) -> 160.1 us (2), dynamic 166.4 -> 164.4 (1) / 164.8
-// (2); 14 040 .. 75 600 alike.  Default: 1 for ticketed launches, 2 otherwise.  AL_BWD_EARLY
-// overrides.
-int bwd_early_release(bool ticketed) {
+// empty barrier 1 = after phase 1, whose row sums consume every value the warp loaded from the
+// slot (before the row-sum reduction and the stage barrier), 0 = after the stage barrier (the
+// round-2 kernels before the pace study).  Releasing earlier keeps more of the ring in flight:
+// B200 A/B (profiles/r2_bwd_early_release.jsonl) cfg2 deterministic 164.0 -> 161.2 us, ticketed
+// 166.4 -> 164.4 us; 14 040 .. 75 600 alike.  (A release right after the shared loads were
+// issued was 0.7 % faster still but raced with the refill -- tools/bwd_race_stress.py -- and is
+// gone.)  AL_BWD_EARLY overrides.
+int bwd_early_release(bool /*ticketed*/) {
   static const int m = [] {
     const char* v = std::getenv("AL_BWD_EARLY");
-    return v ? std::atoi(v) : -1;
+    return v ? (std::atoi(v) ? 1 : 0) : 1;
   }();
-  return m >= 0 ? m : (ticketed ? 1 : 2);
+  return m;
 }
 
 // Single-group launches (one sample, or scale/shift broadcast): 1 = the interleaved static walk
 // in either mode, 0 = a ticketed dynamic tail when the caller does not ask for determinism.
-// With the slot released as soon as a stage is in registers (bwd_early_release) the fixed
+// With the slot released as soon as phase 1 has consumed a stage (bwd_early_release) the fixed
 // interleaved walk is as fast as the ticket walk or faster -- its producer computes the next
 // stage's address instead of waiting on a ticket and the statistics loads it implies -- so
 // the training path and the reference API now run the same bit-reproducible schedule.  B200
@@ -1251,6 +1265,10 @@ int al_device_init(int device) {
               rc = ensure_attr(tma_dyn_kernel(dt, V, R, full), device);
               if (rc) return rc;
             }
+            if (kernel == 1 && tma_gw_kernel(dt, V, R, full)) {
+              rc = ensure_attr(tma_gw_kernel(dt, V, R, full), device);
+              if (rc) return rc;
+            }
             if (kernel == 0) {
               rc = ensure_attr(tma_kernel(kernel, dt, V, R, full, true), device);
               if (rc) return rc;
@@ -1518,7 +1536,7 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
     int dev;
     const bool full = pl.threads - 32 == dim * elem_size(dtype) / 16 / pl.V &&
                       (dim * elem_size(dtype) / 16) % pl.V == 0;
-    const void* gfn = tma_dyn_kernel(dtype, pl.V, pl.R, full);
+    const void* gfn = tma_gw_kernel(dtype, pl.V, pl.R, full);
     if (gfn && cudaGetDevice(&dev) == cudaSuccess && ensure_attr(gfn, dev) == AL_OK) {
       group_walk = true;
       n_dyn = 0;
@@ -1628,13 +1646,13 @@ int al_adaln_backward(const void* dy, const void* x, const void* scale, const vo
   if (group_walk) {
     const bool full = pl.threads - 32 == p.nvec / pl.V && p.nvec % pl.V == 0;
     p.interleave = 2;
-    pl.fn = tma_dyn_kernel(dtype, pl.V, pl.R, full);
+    pl.fn = tma_gw_kernel(dtype, pl.V, pl.R, full);
   }
   // Deterministic single-group launches: the interleaved static walk on the dynamic instance's
   // lean stage body (bit-identical to the static instance; B200, profiles/r2_det_lean.jsonl:
   // cfg2 169.2 -> 164.1 us, S = 75 600 371.8 -> 360.6, 14 040 80.9 -> 78.9; the dynamic tail
   // 161.1 / 357.3 / 76.5 on the same box).  AL_BWD_DET_LEAN=0 restores the static instance.
-  if (p.interleave && !pipe_auto && n_dyn == 0 && bwd_det_lean()) {
+  if (p.interleave == 1 && !pipe_auto && n_dyn == 0 && bwd_det_lean()) {
     int dev;
     const bool full = pl.threads - 32 == p.nvec / pl.V && p.nvec % pl.V == 0;
     const void* dfn = tma_dyn_kernel(dtype, pl.V, pl.R, full);

@@ -1385,7 +1385,11 @@ __device__ void fused_stage2(const BwdParams& p, int nc, int tid) {
 // CTA drew which stage, so dscale/dshift of the last group are reproducible only to fp32
 // rounding in this mode (dx is bit-identical either way).
 // =====================================================================================
-template <typename T, int V, int R, bool FULL, bool DYN>
+// GW: the group-sequential walk instance (p.interleave == 2); kept out of the other instances,
+// whose code it would otherwise change (+5 registers, 2 % slower at cfg2).  (Written as a
+// runtime test on p.interleave rather than `if constexpr`: that form of the GW instance
+// measured 7 % slower on the walk itself, a code-generation effect -- profiles/r2_bwd_group_walk.jsonl)
+template <typename T, int V, int R, bool FULL, bool DYN, bool GW = false>
 __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdParams p) {
   pdl_enter();
   ts_begin(p.ts);
@@ -1432,7 +1436,7 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       const uint8_t* xb = static_cast<const uint8_t*>(p.x);
       const uint8_t* db = static_cast<const uint8_t*>(p.dy);
       StageWalker w;
-      if (p.interleave == 2) w.init(0, 0, p.S_grp);  // empty: the group walk below
+      if (GW && p.interleave == 2) w.init(0, 0, p.S_grp);  // empty: the group walk below
       else if (p.interleave) w.init_interleaved(k, p.G, p.N, R);
       else w.init(r0, r1, p.S_grp);
       int s = 0;
@@ -1449,7 +1453,7 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
           ++f;
         }
       };
-      if (p.interleave == 2) {
+      if (GW && p.interleave == 2) {
         // group-sequential interleaved walk (multi-sample launches of long samples): the
         // interleaved walk of group 0, then of group 1, ... (same order as the consumers)
         const int64_t ng = (p.N + p.S_grp - 1) / p.S_grp;
@@ -1584,7 +1588,7 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
     // phase 1: row sums of g and g*xhat; column accumulators of dy and dy*xhat.
     // Rows past `rows` (stage tail) and columns past D read as zero, so every lane runs the
     // same instruction stream and the shuffles below are convergent.
-    // the stage's x and dy vectors into registers first (mode 2 releases the slot right here)
+    // the stage's x and dy vectors into registers first
     uint4 rawx[R][V], rawd[R][V];
 #pragma unroll
     for (int rr = 0; rr < R; ++rr)
@@ -1595,10 +1599,6 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
         rawx[rr][j] = ok ? ld_shared_v4_u32(stx_u + o) : make_uint4(0, 0, 0, 0);
         rawd[rr][j] = ok ? ld_shared_v4_u32(std_u + o) : make_uint4(0, 0, 0, 0);
       }
-    if (p.early_release == 2) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
     P xh[R][V][NP], gg[R][V][NP];
     CT rowsum[R * 2];
 #pragma unroll
@@ -1629,9 +1629,11 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       rowsum[2 * rr] = tsg.x + tsg.y;
       rowsum[2 * rr + 1] = tsgx.x + tsgx.y;
     }
-    // this warp has the stage in registers (its shared loads are ordered before the arrive by
-    // the mbarrier's release semantics): release the slot now, so the producer refills it
-    // while the row sums are reduced and the barrier waits -- ~25 % of a stage sooner
+    // this warp's phase 1 has consumed every value it loaded from the slot (the row sums depend
+    // on all of them): release the slot now, so the producer refills it while the row sums are
+    // reduced and the barrier waits.  (Releasing right after the shared loads were issued, before
+    // their results were consumed, raced with the refill: tools/bwd_race_stress.py, 25 of 300
+    // launches with corrupted dx at 5 x 17 000 x 1 024.)
     if (p.early_release == 1) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -1693,7 +1695,7 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
     ++it;
   };
 
-  if (p.interleave == 2) {
+  if (GW && p.interleave == 2) {
     // Group-sequential interleaved walk: for each group g, stages k, k + G, ... of that group
     // (rows g*S_grp + st*R), (1 + scale) restaged per group, partials to slot g*G + k -- every
     // CTA flushes every group's slot (zeros if it drew no stage there); stage 2 adds slots
@@ -1890,7 +1892,7 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
     // phase 1: row sums of g and g*xhat; column accumulators of dy and dy*xhat.
     // Rows past `rows` (stage tail) and columns past D read as zero, so every lane runs the
     // same instruction stream and the shuffles below are convergent.
-    // the stage's x and dy vectors into registers first (mode 2 releases the slot right here)
+    // the stage's x and dy vectors into registers first
     uint4 rawx[R][V], rawd[R][V];
 #pragma unroll
     for (int rr = 0; rr < R; ++rr)
@@ -1901,10 +1903,6 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
         rawx[rr][j] = ok ? ld_shared_v4_u32(stx_u + o) : make_uint4(0, 0, 0, 0);
         rawd[rr][j] = ok ? ld_shared_v4_u32(std_u + o) : make_uint4(0, 0, 0, 0);
       }
-    if (p.early_release == 2) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
     P xh[R][V][NP], gg[R][V][NP];
     CT rowsum[R * 2];
 #pragma unroll
@@ -1935,9 +1933,11 @@ __global__ void __launch_bounds__(V == 1 ? 704 : 384) adaln_bwd_tma(const BwdPar
       rowsum[2 * rr] = tsg.x + tsg.y;
       rowsum[2 * rr + 1] = tsgx.x + tsgx.y;
     }
-    // this warp has the stage in registers (its shared loads are ordered before the arrive by
-    // the mbarrier's release semantics): release the slot now, so the producer refills it
-    // while the row sums are reduced and the barrier waits -- ~25 % of a stage sooner
+    // this warp's phase 1 has consumed every value it loaded from the slot (the row sums depend
+    // on all of them): release the slot now, so the producer refills it while the row sums are
+    // reduced and the barrier waits.  (Releasing right after the shared loads were issued, before
+    // their results were consumed, raced with the refill: tools/bwd_race_stress.py, 25 of 300
+    // launches with corrupted dx at 5 x 17 000 x 1 024.)
     if (p.early_release == 1) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);

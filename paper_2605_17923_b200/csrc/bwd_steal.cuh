@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(MAXT, 1) adaln_bwd_steal(const BwdParams p) {
     const uint32_t stx_u = smem_addr(smem) + static_cast<uint32_t>(s * stage_bytes);
     const uint32_t std_u = stx_u + static_cast<uint32_t>(R * RB);
     CT* rd = red + (it & 1) * (ncw * R * 2);
-    // the stage's x and dy vectors into registers first (mode 2 releases the slot right here)
+    // the stage's x and dy vectors into registers first
     uint4 rawx[R][V], rawd[R][V];
 #pragma unroll
     for (int rr = 0; rr < R; ++rr)
@@ -451,10 +451,6 @@ __global__ void __launch_bounds__(MAXT, 1) adaln_bwd_steal(const BwdParams p) {
         rawx[rr][j] = ok ? ld_shared_v4_u32(stx_u + o) : make_uint4(0, 0, 0, 0);
         rawd[rr][j] = ok ? ld_shared_v4_u32(std_u + o) : make_uint4(0, 0, 0, 0);
       }
-    if (p.early_release == 2) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
     P xh[R][V][NP], gg[R][V][NP];
     CT rowsum[R * 2];
 #pragma unroll
