@@ -51,6 +51,19 @@ def _free_port():
     return p
 
 
+def _spawn(fn, world, outdir):
+    """mp.spawn on a fresh 127.0.0.1 port; another process can grab the port between
+    _free_port() and the rendezvous, so an address-in-use failure is retried on a new port."""
+    for attempt in range(3):
+        try:
+            mp.spawn(fn, args=(world, _free_port(), outdir), nprocs=world, join=True)
+            return
+        except Exception as exc:  # noqa: BLE001 - re-raised unless it is the port race
+            msg = str(exc)
+            if attempt == 2 or not ("ddress already in use" in msg or "EADDRINUSE" in msg):
+                raise
+
+
 def _worker(rank, world, port, outdir):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
@@ -93,7 +106,7 @@ def _worker(rank, world, port, outdir):
 @pytest.fixture(scope="module")
 def gloo_results(tmp_path_factory):
     out = tmp_path_factory.mktemp("gloo")
-    mp.spawn(_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True)
+    _spawn(_worker, 2, str(out))
     return [torch.load(out / f"rank{r}.pt") for r in range(2)]
 
 
@@ -170,7 +183,7 @@ def test_world8_dp_step_host_logic(tmp_path):
     draws and the same all-gathered per-rank times, the one flat all-reduce leaves identical
     gradients everywhere, and the bottleneck report has one entry per rank."""
     world = 8
-    mp.spawn(_worker8, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    _spawn(_worker8, world, str(tmp_path))
     res = [torch.load(tmp_path / f"rank{r}.pt", weights_only=False) for r in range(world)]
     for r in res[1:]:
         assert torch.equal(r["grad"], res[0]["grad"])
