@@ -15,7 +15,12 @@ from paper_2605_17923_b200.adaln._ops import backward_workspace_bytes, fused_bac
 
 dev = torch.device("cuda", 0)
 n_iter = int(sys.argv[1]) if len(sys.argv) > 1 else 200
-for b, s, d in [(1, 32760, 5120), (2, 20000, 2048), (2, 18000, 5120), (5, 17000, 1024)]:
+shapes = [(1, 32760, 5120), (2, 20000, 2048), (2, 18000, 5120), (5, 17000, 1024)]
+if os.environ.get("STRESS_ALL"):
+    # + the short-launch pipeline kernel, auto work stealing (multi-sample short), wide rows
+    shapes += [(1, 8000, 5120), (1, 3600, 1024), (3, 7001, 5120), (24, 1560, 5120),
+               (4, 3000, 1536), (1, 12000, 8192)]
+for b, s, d in shapes:
     g = torch.Generator(device="cpu").manual_seed(s)
     x = torch.randn(b, s, d, generator=g).to(torch.bfloat16).to(dev)
     dy = torch.randn(b, s, d, generator=g).to(torch.bfloat16).to(dev)
@@ -26,6 +31,10 @@ for b, s, d in [(1, 32760, 5120), (2, 20000, 2048), (2, 18000, 5120), (5, 17000,
     dsc = torch.empty(b, d, device=dev)
     dsh = torch.empty(b, d, device=dev)
     ws = torch.empty(backward_workspace_bytes(x, sc), dtype=torch.uint8, device=dev)
+    y0 = fused_forward(x, sc, sc)[0].clone()
+    bad_y = 0
+    for _ in range(max(1, n_iter // 5)):
+        bad_y += int(not torch.equal(fused_forward(x, sc, sc)[0], y0))
     bad_dx = bad_dsc = 0
     worst = 0.0
     for i in range(n_iter):
@@ -38,5 +47,5 @@ for b, s, d in [(1, 32760, 5120), (2, 20000, 2048), (2, 18000, 5120), (5, 17000,
         if not torch.equal(dsc, ref[1]):
             bad_dsc += 1
     print(json.dumps({"shape": [b, s, d], "AL_BWD_EARLY": os.environ.get("AL_BWD_EARLY", "default"),
-                      "iters": n_iter, "dx_mismatches": bad_dx, "dscale_mismatches": bad_dsc,
+                      "iters": n_iter, "y_mismatches": bad_y, "dx_mismatches": bad_dx, "dscale_mismatches": bad_dsc,
                       "worst_dx_abs_diff": worst}), flush=True)
