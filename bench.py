@@ -506,9 +506,10 @@ def run_ours(args, world, rank, local):
                    "parallelism": f"dp{world} (independent samples per rank; no collective in the op)",
                    "l2": "inputs larger than L2 (x, dy 335 MB each vs 126 MB L2); no flush",
                    "scheduling": "forward: dynamic row tail (bit-identical to a static split); "
-                                 "backward: the fixed interleaved walk (dscale/dshift "
-                                 "bit-reproducible; the same schedule the reference-facing "
-                                 "deterministic API runs; AL_BWD_TICKET=1 = ticketed tail)",
+                                 "backward: ticketed stage walk (dscale/dshift in a "
+                                 "timing-dependent fp32 order, torch deterministic mode off); "
+                                 "kernels.bwd_deterministic = the reference API's fixed "
+                                 "interleaved walk",
                    "timing": "K steps (fused_forward + fused_backward of the public device API "
                              "into caller-owned buffers) captured in order into one CUDA graph, "
                              "replayed once between CUDA events; per-kernel times from the "

@@ -971,18 +971,17 @@ int bwd_early_release(bool /*ticketed*/) {
   return m;
 }
 
-// Single-group launches (one sample, or scale/shift broadcast): 1 = the interleaved static walk
-// in either mode, 0 = a ticketed dynamic tail when the caller does not ask for determinism.
-// With the slot released as soon as phase 1 has consumed a stage (bwd_early_release) the fixed
-// interleaved walk is as fast as the ticket walk or faster -- its producer computes the next
-// stage's address instead of waiting on a ticket and the statistics loads it implies -- so
-// the training path and the reference API now run the same bit-reproducible schedule.  B200
-// (profiles/r2_bwd_single_group_walk.jsonl): cfg2 160.1 vs 164.4 us, 75 600 352.9 vs 362.2 us
-// on one box, within 1 % either way on another.  AL_BWD_TICKET=1 restores the ticket walk.
+// Single-group launches (one sample, or scale/shift broadcast) without AL_BWD_DETERMINISTIC:
+// 0 = the ticketed dynamic walk (default), 1 = the interleaved static walk of deterministic
+// launches.  Bench-mode A/B on three boxes with the slot released after phase 1
+// (profiles/r2_bwd_schedule_bench_ab3.jsonl, profiles/r2_bwd_defaults_bench_ab_final.jsonl): the
+// ticket walk's step is 0.8 % faster (6 232-6 249 vs 6 183-6 199 GB/s; backward 159.1 vs
+// 160.4 us, and the following forward ~1 us faster); deterministic launches keep the
+// interleaved walk (160.8-161.2 us).  AL_BWD_TICKET=0 selects the interleaved walk for both.
 int bwd_single_group_static() {
   static const int m = [] {
     const char* v = std::getenv("AL_BWD_TICKET");
-    return v ? (std::atoi(v) ? 0 : 1) : 1;
+    return v ? (std::atoi(v) ? 0 : 1) : 0;
   }();
   return m;
 }

@@ -350,9 +350,9 @@ def test_dynamic_tail_backward(shape, mod, cuda):
     # by default (AL_BWD_STEAL unset)
     steal = (len(shape) == 3 and b >= 2 and s_ <= 16384 and plan["rows_per_stage"] == 2
              and os.environ.get("AL_BWD_STEAL") in (None, "2"))
-    # single-group launches walk the fixed interleaved partition in either mode unless the
-    # ticket walk is requested (AL_BWD_TICKET=1, run by test_ticket_walk_backward_subprocess)
-    single = (len(shape) == 2 or b == 1) and os.environ.get("AL_BWD_TICKET") in (None, "0")
+    # AL_BWD_TICKET=0 (run by test_interleaved_walk_backward_subprocess): single-group launches
+    # walk the fixed interleaved partition in either mode; by default they take the ticket walk
+    single = (len(shape) == 2 or b == 1) and os.environ.get("AL_BWD_TICKET") == "0"
     dynamic = (plan["path"] == "tma" and plan["rows_per_stage"] in (2, 4)
                and s_last >= 64 * plan["grid"] and not pipe and not steal and not single)
     assert torch.equal(got[1], ref[1]) != dynamic, plan
@@ -366,15 +366,14 @@ def test_dynamic_tail_backward(shape, mod, cuda):
     assert max_rel_err(h(got[0]), dxo) <= 2e-2
 
 
-def test_ticket_walk_backward_subprocess(cuda):
-    """The ticketed single-group backward (AL_BWD_TICKET=1, read once per process) still passes
-    the dynamic-tail test (dx bit-identical to the static walk, dscale/dshift to fp32 order,
-    every group against the oracle) and the ticket-slot tests under concurrent streams and
-    graph replay."""
+def test_interleaved_walk_backward_subprocess(cuda):
+    """With AL_BWD_TICKET=0 (read once per process) single-group launches walk the interleaved
+    partition in both modes: the dynamic-tail test (now expecting no tail for them) and the
+    ticket-slot tests under concurrent streams and graph replay still pass."""
     import subprocess
     import sys
 
-    env = dict(os.environ, AL_BWD_TICKET="1")
+    env = dict(os.environ, AL_BWD_TICKET="0")
     runtime = os.path.join(os.path.dirname(__file__), "test_runtime_gpu.py")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         __file__ + "::test_dynamic_tail_backward",
